@@ -1,0 +1,178 @@
+/*
+ * mlamr_b200 — C ABI of the B200 multilayer-AMR hot path.
+ *
+ * Plain pointers and sizes only.  All array pointers are DEVICE pointers
+ * unless the parameter name starts with `h_`.  `stream` is a cudaStream_t
+ * passed as void*.  Every entry point is asynchronous on `stream` and
+ * returns 0 on a successful launch; device-side faults (CFL violation,
+ * geometry errors) are reported through the int32 status word described
+ * below, which the host shim maps onto the reference's exception types
+ * (errors.py:4-37 of /root/reference/pkg/src/mlamr).
+ *
+ * Data layout: one pool per level.  Patch p of a level owns a
+ * (ny+4) x (nx+4) row-major block (x fastest, ghost width 2, mesh.py:181-186)
+ * starting at element offset[p]; the 3M state fields (h_0..h_{M-1},
+ * hu_0.., hv_0..) are planes `field_stride` elements apart; bathymetry is
+ * one more plane of the same shape.  Boxes are inclusive global indices
+ * (lo_i, lo_j, hi_i, hi_j) of the patch interior (mesh.py:40-113).
+ *
+ * Owner maps are int32 arrays over a level's index space extended by the
+ * 2-cell frame: cell (i, j) is at [(j + 2) * (level_nx + 4) + (i + 2)].
+ */
+#ifndef MLAMR_B200_H
+#define MLAMR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLAMR_MAX_LAYERS 4
+
+/* status word bits (device int32) */
+#define MLAMR_ST_CFL 1        /* CflViolationError  (physics.py:342-347) */
+#define MLAMR_ST_GEOMETRY 2   /* GeometryError      (refine.py:210-225)  */
+#define MLAMR_ST_NONFINITE 4  /* NumericalAbortError (driver.py:286-297) */
+
+/* boundary kinds, per side in the order left, right, bottom, top */
+#define MLAMR_BC_WALL 0
+#define MLAMR_BC_OUTFLOW 1
+
+typedef struct mlamr_params {
+    int32_t num_layers;                 /* M (1..4)                           */
+    int32_t pad_;
+    double gravity;                     /* g                                  */
+    double dry_tolerance;               /* tol                                */
+    double densities[MLAMR_MAX_LAYERS]; /* top to bottom (state.py:19-53)     */
+} mlamr_params;
+
+typedef struct mlamr_level {
+    int32_t num_patches;
+    int32_t num_layers;
+    int32_t level_nx, level_ny;   /* level index space                   */
+    double dx, dy;
+    int64_t field_stride;         /* elements between state planes       */
+    const int32_t *box;           /* [P*4]                               */
+    const int64_t *offset;        /* [P]                                 */
+    double *state;                /* [3M * field_stride]                 */
+    double *bathy;                /* [field_stride]                      */
+    const int32_t *own;           /* interior-owner map (last wins)      */
+    const int32_t *gown;          /* frame-owner map (first wins) or NULL */
+} mlamr_level;
+
+/* ---- library ------------------------------------------------------------ */
+/* Number of exported entry points / a version string (for smoke checks). */
+int mlamr_version(void);
+const char *mlamr_build_info(void);
+
+/* ---- owner maps (replace the O(P^2) box scans of ghost.py:186-196,
+ *      regrid.py:311-323, coarsen.py:57-75) -------------------------------
+ * Paint the boxes of a level into an owner map that was pre-set to -1.
+ * grow = 0 paints interiors, 2 interiors plus the ghost frame; first_wins
+ * selects the smallest patch index (gather's ghost fallback, ghost.py:
+ * 73-84) instead of the largest (later interiors overwrite, ghost.py:64-72).
+ * r_x/r_y > 1 paints coarsened boxes into the parent's index space.
+ * max_cells bounds the painted cells per box (grid sizing). */
+int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int32_t *box,
+                      int num_patches, int grow, int first_wins, int r_x, int r_y,
+                      int max_cells, void *stream);
+
+/* ---- K1: batched patch step (physics.step_patch, physics.py:330-386) -----
+ * Reads `src_state` (ghosts filled), writes the stepped interior into
+ * `dst_state`.  `tiles` is an int32 [n_tiles*3] work list (patch, j0, i0)
+ * of 16x32 interior tiles.  Per-patch observed speeds of the pre-step state
+ * go to `speed_bits` (int64 bit patterns, pre-set to -1 = all dry);
+ * per-tile partials (sum of clipped negative depth per layer, hyperbolicity
+ * fixes, wet-prefix repairs) to `tile_acc` [n_tiles * (M + 2)].
+ * Does nothing when *status != 0. */
+int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
+               const int32_t *tiles, int n_tiles, double dt, int y_first,
+               mlamr_params prm, long long *speed_bits, double *tile_acc,
+               const int32_t *status, void *stream);
+
+/* CFL guard (physics.py:342-347) + deterministic reduction of a step's
+ * partials into acc[M + 2].  A patch whose speed*dt/min(dx,dy) > 1 gets its
+ * interior restored from src (the reference raises before touching it),
+ * MLAMR_ST_CFL is set and the smallest such patch index is atomically
+ * min-ed into *bad_patch. */
+int mlamr_step_finalize(mlamr_level lv, const double *src_state, double *dst_state,
+                        const int32_t *tiles, int n_tiles, double dt,
+                        mlamr_params prm, const long long *speed_bits,
+                        const double *tile_acc, double *acc, int32_t *status,
+                        int32_t *bad_patch, void *stream);
+
+/* ---- K6: per-patch observed max wave speed (physics.py:261-278) --------- */
+int mlamr_max_speed_tiles(mlamr_level lv, const double *state, const int32_t *tiles,
+                          int n_tiles, mlamr_params prm, long long *speed_bits,
+                          void *stream);
+
+/* ---- K2: ghost filling (ghost.py:145-197, driver.py:157-190) -------------
+ * Coarse interpolation from the parent level, time-blended as
+ * (1-theta)*old + theta*new when `parent_old_state` (the stash) is given
+ * (ghost.py:68-71); then sibling copies; then physical BCs.  `parent` NULL
+ * = coarsest level.  `bcs` is a HOST int32[4] (left, right, bottom, top). */
+int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent,
+                      const double *parent_old_state, double theta,
+                      int r_x, int r_y, const int32_t *bcs,
+                      mlamr_params prm, const int32_t *status, void *stream);
+
+/* Patch bathymetry (frame included) from a level-wide array of in-domain
+ * values, then ghost.apply_bathymetry_bcs (ghost.py:118-129). */
+int mlamr_fill_bathymetry(mlamr_level lv, const double *level_bathy,
+                          const int32_t *bcs, void *stream);
+
+/* ---- K4: coarsening (coarsen.average_down, coarsen.py:30-76) ------------
+ * Block means of every fine patch written over the coarse interiors that
+ * own them (coarse.own); per-(fine patch, block) mass-change partials
+ * [P_fine * blocks_per_patch * M]. */
+int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x, int r_y,
+                       mlamr_params prm, double *patch_delta, int blocks_per_patch,
+                       const int32_t *status, void *stream);
+
+/* ---- K3 + K5: regrid data movement (regrid.py:270-353) -------------------
+ * Every new-patch interior cell is copied from the old patch covering it
+ * (old.own), else refined from the parent's interiors (gather with
+ * include_ghosts=False).  Refine-delta partials [P_new * blocks * M]. */
+int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_level parent,
+                      int r_x, int r_y, mlamr_params prm, double *refine_delta,
+                      int blocks_per_patch, int32_t *status, void *stream);
+/* Derefine delta (regrid.py:329-348); new_child = the new patches'
+ * coarsened owner map in the parent's index space. */
+int mlamr_derefine_delta(mlamr_level oldlv, mlamr_level parent, const int32_t *new_child,
+                         int r_x, int r_y, mlamr_params prm, double *derefine_delta,
+                         int blocks_per_patch, void *stream);
+
+/* Standalone interpolate_state (refine.py:158-190) over a gathered coarse
+ * array [M][cny][cnx] with availability mask; fine outputs [M][fny][fnx]. */
+int mlamr_interpolate_box(int M, const double *ch, const double *chu, const double *chv,
+                          const double *cb, const uint8_t *cavail,
+                          int clo_i, int clo_j, int cnx, int cny,
+                          int flo_i, int flo_j, int fnx, int fny,
+                          const double *fb, int r_x, int r_y, mlamr_params prm,
+                          double *oh, double *ohu, double *ohv, int32_t *status,
+                          void *stream);
+
+/* ---- K6: level reductions (driver.py:138-153, 286-297) ------------------
+ * Per-(patch, block) uncovered-interior depth sums [P * blocks * M] (child
+ * = coarsened owner map of the finer level in this level's index space, or
+ * NULL) and a non-finite scan of interiors (`interior_state`) and frames
+ * (`ghost_state`) that sets MLAMR_ST_NONFINITE. */
+int mlamr_level_reduce(mlamr_level lv, const double *interior_state,
+                       const double *ghost_state, const int32_t *child,
+                       double *patch_mass, int blocks_per_patch,
+                       int32_t *status, void *stream);
+
+/* Reference flag rule, per-cell part (regrid.flag_cells, regrid.py:58-101):
+ * cell_bits over the level index space (no frame): bit0 amplitude flag
+ * |eta_m - eta_rest_m| > wave_tol_m, bit(1+m) layer m wet, bit7 covered.
+ * The dilations are applied by the host. */
+int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm,
+                     const double *eta_rest, const double *wave_tol,
+                     uint8_t *cell_bits, int blocks_per_patch, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MLAMR_B200_H */

@@ -1,0 +1,650 @@
+// K2 ghost filling, K3/K5 regrid data movement, K4 coarsening, K6 level
+// reductions, owner-map painting and the reference flag rule.
+//
+// All batched over every patch of a level in one launch.  Patch-to-patch
+// relations (siblings, parents, old/new patches, fine/coarse overlaps) are
+// resolved through int32 owner maps over each level's index space instead
+// of the reference's O(P^2) box scans (ghost.py:186-196, regrid.py:311-323,
+// coarsen.py:57-75); the painting order reproduces the reference's
+// list-order precedence (interiors: last wins; ghost fallback: first wins).
+
+#include "interp.cuh"
+
+namespace mlamr {
+
+constexpr int NTA = 256;
+
+// ---------------------------------------------------------------------------
+// owner maps
+// ---------------------------------------------------------------------------
+__global__ void k_paint(int32_t *map, int map_nx, int map_ny, const int32_t *box, int grow,
+                        int first_wins, int r_x, int r_y) {
+    const int p = blockIdx.y;
+    const int32_t *b = box + 4 * p;
+    int lo_i = b[0], lo_j = b[1], hi_i = b[2], hi_j = b[3];
+    if (r_x > 1 || r_y > 1) {  // coarsened footprint (aligned boxes)
+        lo_i = floordiv(lo_i, r_x);
+        lo_j = floordiv(lo_j, r_y);
+        hi_i = floordiv(hi_i + 1, r_x) - 1;
+        hi_j = floordiv(hi_j + 1, r_y) - 1;
+    }
+    lo_i -= grow; lo_j -= grow; hi_i += grow; hi_j += grow;
+    const int nx = hi_i - lo_i + 1, ny = hi_j - lo_j + 1;
+    const int W = map_nx + 2 * MLAMR_G;
+    for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nx * ny; idx += gridDim.x * blockDim.x) {
+        const int j = lo_j + idx / nx, i = lo_i + idx % nx;
+        if (i < -MLAMR_G || j < -MLAMR_G || i >= map_nx + MLAMR_G || j >= map_ny + MLAMR_G) continue;
+        int32_t *cell = map + (int64_t)(j + MLAMR_G) * W + (i + MLAMR_G);
+        if (first_wins) {
+            // map pre-set to -1: take the smallest index
+            int cur = *cell;
+            while (cur < 0 || p < cur) {
+                const int prev = atomicCAS(cell, cur, p);
+                if (prev == cur) break;
+                cur = prev;
+            }
+        } else {
+            atomicMax(cell, p);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2: ghost filling (ghost.fill_ghosts, ghost.py:156-197)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void ghost_cell_of(int idx, int NX, int NY, int ny, int &J, int &I) {
+    if (idx < 2 * NX) {  // bottom rows
+        J = idx / NX;
+        I = idx % NX;
+    } else if (idx < 4 * NX) {  // top rows
+        const int q = idx - 2 * NX;
+        J = NY - 2 + q / NX;
+        I = q % NX;
+    } else {  // left/right columns on interior rows
+        const int q = idx - 4 * NX;
+        J = MLAMR_G + q / 4;
+        const int s = q % 4;
+        I = (s == 0) ? 0 : (s == 1) ? 1 : (s == 2) ? NX - 2 : NX - 1;
+    }
+}
+
+// one side of the physical BCs (ghost._mirror_or_copy, ghost.py:89-106)
+template <int M>
+__device__ void bc_side(double *st, int64_t FS, int64_t off, int NX, int NY, int side, int kind,
+                        double *bathy_only) {
+    const int t = threadIdx.x;
+    const bool xs = side < 2;
+    const int n_lines = xs ? NY : NX;
+    const int nq = (bathy_only != nullptr) ? 1 : 3 * M;
+    for (int idx = t; idx < n_lines * 2 * nq; idx += NTA) {
+        const int q = idx / (n_lines * 2);
+        const int rem = idx - q * n_lines * 2;
+        const int line = rem >> 1;
+        const int k = rem & 1;
+        double *a = (bathy_only != nullptr) ? bathy_only : st + q * FS;
+        double sign = 1.0;
+        if (bathy_only == nullptr) {
+            const int fam = q / M;  // 0 h, 1 hu, 2 hv
+            if (fam == 1 && xs) sign = -1.0;
+            if (fam == 2 && !xs) sign = -1.0;
+        }
+        int dst_rc, src_rc;
+        const int g = MLAMR_G;
+        if (side == 0) {         // left: col g-1-k <- col g+k | col g
+            dst_rc = g - 1 - k; src_rc = (kind == MLAMR_BC_WALL) ? g + k : g;
+        } else if (side == 1) {  // right: col NX-g+k <- col NX-g-1-k | col NX-g-1
+            dst_rc = NX - g + k; src_rc = (kind == MLAMR_BC_WALL) ? NX - g - 1 - k : NX - g - 1;
+        } else if (side == 2) {  // bottom rows
+            dst_rc = g - 1 - k; src_rc = (kind == MLAMR_BC_WALL) ? g + k : g;
+        } else {                 // top rows
+            dst_rc = NY - g + k; src_rc = (kind == MLAMR_BC_WALL) ? NY - g - 1 - k : NY - g - 1;
+        }
+        int64_t d, s;
+        if (xs) {
+            d = off + (int64_t)line * NX + dst_rc;
+            s = off + (int64_t)line * NX + src_rc;
+        } else {
+            d = off + (int64_t)dst_rc * NX + line;
+            s = off + (int64_t)src_rc * NX + line;
+        }
+        a[d] = (kind == MLAMR_BC_WALL) ? sign * a[s] : a[s];
+    }
+}
+
+template <int M>
+__device__ void apply_bcs(const mlamr_level &lv, const PatchView &pv, const int4 bcs,
+                          double *bathy_only) {
+    // sides touching the level box, x sides first (ghost.py:109-121)
+    const bool touch[4] = {pv.lo_i == 0, pv.lo_i + pv.nx == lv.level_nx, pv.lo_j == 0,
+                           pv.lo_j + pv.ny == lv.level_ny};
+    const int kinds[4] = {bcs.x, bcs.y, bcs.z, bcs.w};
+#pragma unroll 1
+    for (int side = 0; side < 4; ++side) {
+        if (!touch[side]) continue;
+        bc_side<M>(lv.state, lv.field_stride, pv.off, pv.NX, pv.NY, side, kinds[side], bathy_only);
+        __syncthreads();
+    }
+}
+
+template <int M>
+__global__ void __launch_bounds__(NTA) k_fill_ghosts(mlamr_level lv, mlamr_level par, int has_parent,
+                                                     const double *par_old, double theta, int r_x,
+                                                     int r_y, int4 bcs, mlamr_params prm,
+                                                     const int32_t *status) {
+    if (status != nullptr && *status != 0) return;
+    const int p = blockIdx.x;
+    const PatchView pv = patch_view(lv, p);
+    const int64_t FS = lv.field_stride;
+    const double tol = prm.dry_tolerance;
+    const int nghost = 4 * pv.NX + 4 * pv.ny;
+    for (int idx = threadIdx.x; idx < nghost; idx += NTA) {
+        int J, I;
+        ghost_cell_of(idx, pv.NX, pv.NY, pv.ny, J, I);
+        const int gi = pv.lo_i - MLAMR_G + I, gj = pv.lo_j - MLAMR_G + J;
+        if (gi < 0 || gj < 0 || gi >= lv.level_nx || gj >= lv.level_ny) continue;
+        const int64_t k = pv.off + (int64_t)J * pv.NX + I;
+        const int sib = owner_at(lv.own, lv.level_nx, lv.level_ny, gi, gj);
+        if (sib >= 0 && sib != p) {
+            const int32_t *b = lv.box + 4 * sib;
+            const int SNX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+            const int64_t ks = lv.offset[sib] + (int64_t)(gj - b[1] + MLAMR_G) * SNX + (gi - b[0] + MLAMR_G);
+#pragma unroll
+            for (int q = 0; q < 3 * M; ++q) lv.state[q * FS + k] = lv.state[q * FS + ks];
+        } else if (has_parent) {
+            const int pi = floordiv(gi, r_x), pj = floordiv(gj, r_y);
+            Coarse5<M> c;
+            gather5<M>(par, par.state, par_old, theta, true, pi, pj, c);
+            Slopes<M> s;
+            parent_slopes<M>(c, tol, s);
+            double h[M], hu[M], hv[M];
+            fine_cell<M>(s, child_offset(gi, pi, r_x), child_offset(gj, pj, r_y), lv.bathy[k], tol, h, hu, hv);
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                lv.state[m * FS + k] = h[m];
+                lv.state[(M + m) * FS + k] = hu[m];
+                lv.state[(2 * M + m) * FS + k] = hv[m];
+            }
+        }
+    }
+    __syncthreads();
+    apply_bcs<M>(lv, pv, bcs, nullptr);
+}
+
+__global__ void __launch_bounds__(NTA) k_fill_bathy(mlamr_level lv, const double *level_bathy, int4 bcs) {
+    const int p = blockIdx.x;
+    const PatchView pv = patch_view(lv, p);
+    for (int idx = threadIdx.x; idx < pv.NX * pv.NY; idx += NTA) {
+        const int J = idx / pv.NX, I = idx % pv.NX;
+        const int gi = pv.lo_i - MLAMR_G + I, gj = pv.lo_j - MLAMR_G + J;
+        double v = 0.0;
+        if (gi >= 0 && gj >= 0 && gi < lv.level_nx && gj < lv.level_ny)
+            v = level_bathy[(int64_t)gj * lv.level_nx + gi];
+        lv.bathy[pv.off + idx] = v;
+    }
+    __syncthreads();
+    apply_bcs<1>(lv, pv, bcs, lv.bathy);
+}
+
+// ---------------------------------------------------------------------------
+// K4: coarsening (coarsen.average_down, coarsen.py:30-76)
+// One thread per coarse cell of a fine patch's footprint.
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_level coarse, int r_x,
+                                                      int r_y, mlamr_params prm, double *patch_delta,
+                                                      const int32_t *status) {
+    __shared__ double red[NTA];
+    if (status != nullptr && *status != 0) return;
+    const int p = blockIdx.y;
+    const PatchView fv = patch_view(fine, p);
+    const int cnx = fv.nx / r_x, cny = fv.ny / r_y;
+    const int clo_i = floordiv(fv.lo_i, r_x), clo_j = floordiv(fv.lo_j, r_y);
+    const int64_t FF = fine.field_stride, CF = coarse.field_stride;
+    const double tol = prm.dry_tolerance;
+    const double inv_n = (double)(r_x * r_y);
+    double dsum[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) dsum[m] = 0.0;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
+        const int J = idx / cnx, I = idx % cnx;
+        const int ci = clo_i + I, cj = clo_j + J;
+        const int o = owner_at(coarse.own, coarse.level_nx, coarse.level_ny, ci, cj);
+        if (o < 0) continue;
+        double avg[3][M];
+#pragma unroll
+        for (int f = 0; f < 3; ++f)
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const double *a = fine.state + (f * M + m) * FF + fv.off;
+                double s = 0.0;
+                for (int q = 0; q < r_y; ++q) {
+                    const double *row = a + (int64_t)(MLAMR_G + J * r_y + q) * fv.NX + (MLAMR_G + I * r_x);
+                    double rs = row[0];
+                    for (int pp = 1; pp < r_x; ++pp) rs = rs + row[pp];
+                    s = (q == 0) ? rs : s + rs;
+                }
+                avg[f][m] = s / inv_n;
+            }
+        const int32_t *b = coarse.box + 4 * o;
+        const int CNX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+        const int64_t kc = coarse.offset[o] + (int64_t)(cj - b[1] + MLAMR_G) * CNX + (ci - b[0] + MLAMR_G);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            if (avg[0][m] <= tol) {
+                avg[1][m] = 0.0;
+                avg[2][m] = 0.0;
+            }
+            dsum[m] = dsum[m] + (avg[0][m] - coarse.state[m * CF + kc]);
+            coarse.state[m * CF + kc] = avg[0][m];
+            coarse.state[(M + m) * CF + kc] = avg[1][m];
+            coarse.state[(2 * M + m) * CF + kc] = avg[2][m];
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const double s = block_sum<NTA>(dsum[m], red);
+        if (threadIdx.x == 0) patch_delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3 + K5: regrid data movement (regrid.rebuild_child_level, regrid.py:270-353)
+// One thread per coarse cell of a new patch's footprint: either copy its
+// r_x*r_y children from the old patch covering them, or refine them from
+// the parent's interiors (gather include_ghosts=False, regrid.py:295-300).
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
+                                                     int r_x, int r_y, mlamr_params prm,
+                                                     double *refine_delta, int32_t *status) {
+    __shared__ double red[NTA];
+    const int p = blockIdx.y;
+    const PatchView nv = patch_view(nl, p);
+    const int cnx = nv.nx / r_x, cny = nv.ny / r_y;
+    const int clo_i = floordiv(nv.lo_i, r_x), clo_j = floordiv(nv.lo_j, r_y);
+    const int64_t NF = nl.field_stride, OF = ol.field_stride;
+    const double tol = prm.dry_tolerance;
+    const double af = nl.dx * nl.dy, ac = par.dx * par.dy;
+    double dsum[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) dsum[m] = 0.0;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
+        const int J = idx / cnx, I = idx % cnx;
+        const int ci = clo_i + I, cj = clo_j + J;
+        const int fi0 = ci * r_x, fj0 = cj * r_y;
+        const int o = owner_at(ol.own, ol.level_nx, ol.level_ny, fi0, fj0);
+        if (o >= 0) {
+            const int32_t *b = ol.box + 4 * o;
+            const int ONX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+            for (int q = 0; q < r_y; ++q)
+                for (int pp = 0; pp < r_x; ++pp) {
+                    const int fi = fi0 + pp, fj = fj0 + q;
+                    const int64_t ks = ol.offset[o] + (int64_t)(fj - b[1] + MLAMR_G) * ONX + (fi - b[0] + MLAMR_G);
+                    const int64_t kd = nv.off + (int64_t)(fj - nv.lo_j + MLAMR_G) * nv.NX + (fi - nv.lo_i + MLAMR_G);
+#pragma unroll
+                    for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + kd] = ol.state[f * OF + ks];
+                }
+            continue;
+        }
+        Coarse5<M> c;
+        gather5<M>(par, par.state, nullptr, 0.0, false, ci, cj, c);
+        if (!c.avail[0]) {  // coarse data under the region is incomplete (refine.py:222-225)
+            atomicOr(status, MLAMR_ST_GEOMETRY);
+            continue;
+        }
+        Slopes<M> s;
+        parent_slopes<M>(c, tol, s);
+        double fine_sum[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) fine_sum[m] = 0.0;
+        for (int q = 0; q < r_y; ++q)
+            for (int pp = 0; pp < r_x; ++pp) {
+                const int fi = fi0 + pp, fj = fj0 + q;
+                const int64_t kd = nv.off + (int64_t)(fj - nv.lo_j + MLAMR_G) * nv.NX + (fi - nv.lo_i + MLAMR_G);
+                double h[M], hu[M], hv[M];
+                fine_cell<M>(s, child_offset(fi, ci, r_x), child_offset(fj, cj, r_y), nl.bathy[kd], tol, h, hu, hv);
+#pragma unroll
+                for (int m = 0; m < M; ++m) {
+                    nl.state[m * NF + kd] = h[m];
+                    nl.state[(M + m) * NF + kd] = hu[m];
+                    nl.state[(2 * M + m) * NF + kd] = hv[m];
+                    fine_sum[m] = fine_sum[m] + h[m];
+                }
+            }
+#pragma unroll
+        for (int m = 0; m < M; ++m) dsum[m] = dsum[m] + ((fine_sum[m] * af) - (c.h[0][m] * ac));
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const double s = block_sum<NTA>(dsum[m], red);
+        if (threadIdx.x == 0) refine_delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
+    }
+}
+
+// derefine delta (regrid.py:329-348): coarse cells covered by an old patch
+// but by no new one: coarse mass minus the discarded fine mass.
+template <int M>
+__global__ void __launch_bounds__(NTA) k_derefine(mlamr_level ol, mlamr_level par, const int32_t *new_child,
+                                                  int r_x, int r_y, double *delta) {
+    __shared__ double red[NTA];
+    const int p = blockIdx.y;
+    const PatchView ov = patch_view(ol, p);
+    const int cnx = ov.nx / r_x, cny = ov.ny / r_y;
+    const int clo_i = floordiv(ov.lo_i, r_x), clo_j = floordiv(ov.lo_j, r_y);
+    const int64_t OF = ol.field_stride, PF = par.field_stride;
+    const double af = ol.dx * ol.dy, ac = par.dx * par.dy;
+    double dsum[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) dsum[m] = 0.0;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
+        const int J = idx / cnx, I = idx % cnx;
+        const int ci = clo_i + I, cj = clo_j + J;
+        if (owner_at(new_child, par.level_nx, par.level_ny, ci, cj) >= 0) continue;
+        const int o = owner_at(par.own, par.level_nx, par.level_ny, ci, cj);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            double fs = 0.0;
+            for (int q = 0; q < r_y; ++q)
+                for (int pp = 0; pp < r_x; ++pp)
+                    fs = fs + ol.state[m * OF + ov.off + (int64_t)(MLAMR_G + J * r_y + q) * ov.NX + (MLAMR_G + I * r_x + pp)];
+            double cv = 0.0;
+            if (o >= 0) {
+                const int32_t *b = par.box + 4 * o;
+                const int CNX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+                cv = par.state[m * PF + par.offset[o] + (int64_t)(cj - b[1] + MLAMR_G) * CNX + (ci - b[0] + MLAMR_G)];
+            }
+            dsum[m] = dsum[m] + ((cv * ac) - (fs * af));
+        }
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const double s = block_sum<NTA>(dsum[m], red);
+        if (threadIdx.x == 0) delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// standalone interpolate_state over a gathered coarse array (drop-in shim)
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void k_interp_box(const double *ch, const double *chu, const double *chv, const double *cb,
+                             const uint8_t *cavail, int clo_i, int clo_j, int cnx, int cny, int flo_i,
+                             int flo_j, int fnx, int fny, const double *fb, int r_x, int r_y,
+                             double tol, double *oh, double *ohu, double *ohv, int32_t *status) {
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx >= fnx * fny) return;
+    const int fj = idx / fnx, fi = idx % fnx;
+    const int gi = flo_i + fi, gj = flo_j + fj;
+    const int pi = floordiv(gi, r_x), pj = floordiv(gj, r_y);
+    const int ci = pi - clo_i, cj = pj - clo_j;
+    if (ci < 0 || cj < 0 || ci >= cnx || cj >= cny) {
+        atomicOr(status, MLAMR_ST_GEOMETRY);
+        return;
+    }
+    const int64_t cplane = (int64_t)cnx * cny;
+    Coarse5<M> c;
+    const int di[5] = {0, -1, 1, 0, 0}, dj[5] = {0, 0, 0, -1, 1};
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        const int x = ci + di[q], y = cj + dj[q];
+        const bool in = x >= 0 && y >= 0 && x < cnx && y < cny;
+        const int64_t k = (int64_t)y * cnx + x;
+        c.avail[q] = in && cavail[k];
+        c.B[q] = in ? cb[k] : 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            c.h[q][m] = in ? ch[m * cplane + k] : 0.0;
+            c.hu[q][m] = in ? chu[m * cplane + k] : 0.0;
+            c.hv[q][m] = in ? chv[m * cplane + k] : 0.0;
+        }
+    }
+    // slopes are zero at the gathered array border (refine.py:88-91): an
+    // out-of-array neighbour is treated as unusable
+    Slopes<M> s;
+    parent_slopes<M>(c, tol, s);
+    double h[M], hu[M], hv[M];
+    fine_cell<M>(s, child_offset(gi, pi, r_x), child_offset(gj, pj, r_y), fb[idx], tol, h, hu, hv);
+    const int64_t fplane = (int64_t)fnx * fny;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        oh[m * fplane + idx] = h[m];
+        ohu[m * fplane + idx] = hu[m];
+        ohv[m * fplane + idx] = hv[m];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: composite mass partials + non-finite scan (driver.py:138-153, 286-297)
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const double *interior,
+                                                      const double *ghosts, const int32_t *child,
+                                                      int child_rx, int child_ry, double *patch_mass,
+                                                      int32_t *status) {
+    __shared__ double red[NTA];
+    __shared__ int bad;
+    const int p = blockIdx.y;
+    const PatchView pv = patch_view(lv, p);
+    const int64_t FS = lv.field_stride;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    double msum[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) msum[m] = 0.0;
+    int nonfinite = 0;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < pv.NX * pv.NY; idx += gridDim.x * NTA) {
+        const int J = idx / pv.NX, I = idx % pv.NX;
+        const bool inner = J >= MLAMR_G && J < pv.NY - MLAMR_G && I >= MLAMR_G && I < pv.NX - MLAMR_G;
+        const double *st = inner ? interior : ghosts;
+        const int64_t k = pv.off + idx;
+        for (int q = 0; q < 3 * M; ++q)
+            if (!isfinite(st[q * FS + k])) nonfinite = 1;
+        if (inner) {
+            const int gi = pv.lo_i + I - MLAMR_G, gj = pv.lo_j + J - MLAMR_G;
+            const bool covered = child != nullptr && owner_at(child, lv.level_nx, lv.level_ny, gi, gj) >= 0;
+            if (!covered) {
+#pragma unroll
+                for (int m = 0; m < M; ++m) msum[m] = msum[m] + interior[m * FS + k];
+            }
+        }
+    }
+    if (nonfinite) atomicOr(&bad, 1);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const double s = block_sum<NTA>(msum[m], red);
+        if (threadIdx.x == 0) patch_mass[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
+    }
+    if (threadIdx.x == 0 && bad) atomicOr(status, MLAMR_ST_NONFINITE);
+}
+
+// ---------------------------------------------------------------------------
+// reference flag rule, per cell part (regrid.flag_cells, regrid.py:58-101)
+// bit0 amplitude flag, bit(1+m) wet layer m, bit7 covered.
+// ---------------------------------------------------------------------------
+template <int M>
+__global__ void __launch_bounds__(NTA) k_flag_cells(mlamr_level lv, const double *st, mlamr_params prm,
+                                                    const double *eta_rest, const double *wave_tol,
+                                                    uint8_t *bits) {
+    const int p = blockIdx.y;
+    const PatchView pv = patch_view(lv, p);
+    const int64_t FS = lv.field_stride;
+    const double tol = prm.dry_tolerance;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < pv.nx * pv.ny; idx += gridDim.x * NTA) {
+        const int J = idx / pv.nx, I = idx % pv.nx;
+        const int64_t k = pv.off + (int64_t)(J + MLAMR_G) * pv.NX + (I + MLAMR_G);
+        const double B = lv.bathy[k];
+        // rest depths from the rest surfaces (scenario.py:73-96, state.py:72-101)
+        double hr[M], h[M];
+        double bhat = 0.0 + B;
+#pragma unroll
+        for (int m = M - 1; m >= 0; --m) {
+            const double d = eta_rest[m] - bhat;
+            hr[m] = np_max(d, 0.0);
+            bhat = bhat + hr[m];
+            h[m] = st[m * FS + k];
+        }
+        uint8_t out = 0x80;
+        double acc = 0.0, accr = 0.0;
+#pragma unroll
+        for (int m = M - 1; m >= 0; --m) {
+            acc = (m == M - 1) ? h[m] : acc + h[m];
+            accr = (m == M - 1) ? hr[m] : accr + hr[m];
+            const double eta = acc + B;
+            const double er = accr + B;
+            if (fabs(eta - er) > wave_tol[m]) out |= 1;
+            if (h[m] > tol) out |= (uint8_t)(2u << m);
+        }
+        bits[(int64_t)(pv.lo_j + J) * lv.level_nx + (pv.lo_i + I)] = out;
+    }
+}
+
+template <typename F>
+static int dispatch_m(int M, F &&f) {
+    switch (M) {
+        case 1: f(std::integral_constant<int, 1>{}); return 0;
+        case 2: f(std::integral_constant<int, 2>{}); return 0;
+        case 3: f(std::integral_constant<int, 3>{}); return 0;
+        default: return -1;
+    }
+}
+
+static inline int blocks_for(int64_t n, int maxb = 64) {
+    int64_t b = (n + NTA - 1) / NTA;
+    if (b < 1) b = 1;
+    if (b > maxb) b = maxb;
+    return (int)b;
+}
+
+}  // namespace mlamr
+
+#include <type_traits>
+
+using namespace mlamr;
+
+extern "C" int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int32_t *box,
+                                 int num_patches, int grow, int first_wins, int r_x, int r_y,
+                                 int max_cells, void *stream) {
+    if (num_patches <= 0) return 0;
+    dim3 grid(blocks_for(max_cells, 256), num_patches);
+    k_paint<<<grid, NTA, 0, as_stream(stream)>>>(map, map_nx, map_ny, box, grow, first_wins, r_x, r_y);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent, const double *parent_old_state,
+                                 double theta, int r_x, int r_y, const int32_t *bcs, mlamr_params prm,
+                                 const int32_t *status, void *stream) {
+    if (lv.num_patches <= 0) return 0;
+    mlamr_level par = parent ? *parent : lv;
+    const int4 b = make_int4(bcs[0], bcs[1], bcs[2], bcs[3]);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_fill_ghosts<M><<<lv.num_patches, NTA, 0, st>>>(lv, par, parent != nullptr, parent_old_state, theta,
+                                                         r_x, r_y, b, prm, status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_fill_bathymetry(mlamr_level lv, const double *level_bathy, const int32_t *bcs,
+                                     void *stream) {
+    if (lv.num_patches <= 0) return 0;
+    const int4 b = make_int4(bcs[0], bcs[1], bcs[2], bcs[3]);
+    k_fill_bathy<<<lv.num_patches, NTA, 0, as_stream(stream)>>>(lv, level_bathy, b);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x, int r_y, mlamr_params prm,
+                                  double *patch_delta, int blocks_per_patch, const int32_t *status,
+                                  void *stream) {
+    if (fine.num_patches <= 0) return 0;
+    dim3 grid(blocks_per_patch, fine.num_patches);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_average_down<M><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_level parent, int r_x, int r_y,
+                                 mlamr_params prm, double *refine_delta, int blocks_per_patch,
+                                 int32_t *status, void *stream) {
+    if (newlv.num_patches <= 0) return 0;
+    dim3 grid(blocks_per_patch, newlv.num_patches);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_regrid_fill<M><<<grid, NTA, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_derefine_delta(mlamr_level oldlv, mlamr_level parent, const int32_t *new_child,
+                                    int r_x, int r_y, mlamr_params prm, double *derefine_delta,
+                                    int blocks_per_patch, void *stream) {
+    if (oldlv.num_patches <= 0) return 0;
+    dim3 grid(blocks_per_patch, oldlv.num_patches);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_interpolate_box(int M, const double *ch, const double *chu, const double *chv,
+                                     const double *cb, const uint8_t *cavail, int clo_i, int clo_j, int cnx,
+                                     int cny, int flo_i, int flo_j, int fnx, int fny, const double *fb,
+                                     int r_x, int r_y, mlamr_params prm, double *oh, double *ohu,
+                                     double *ohv, int32_t *status, void *stream) {
+    const int n = fnx * fny;
+    if (n <= 0) return 0;
+    cudaStream_t st = as_stream(stream);
+    const int nb = (n + 127) / 128;
+    int rc = dispatch_m(M, [&](auto Mc) {
+        constexpr int MM = decltype(Mc)::value;
+        k_interp_box<MM><<<nb, 128, 0, st>>>(ch, chu, chv, cb, cavail, clo_i, clo_j, cnx, cny, flo_i, flo_j,
+                                             fnx, fny, fb, r_x, r_y, prm.dry_tolerance, oh, ohu, ohv, status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_level_reduce(mlamr_level lv, const double *interior_state, const double *ghost_state,
+                                  const int32_t *child, double *patch_mass, int blocks_per_patch,
+                                  int32_t *status, void *stream) {
+    if (lv.num_patches <= 0) return 0;
+    dim3 grid(blocks_per_patch, lv.num_patches);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(lv.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_level_reduce<M><<<grid, NTA, 0, st>>>(lv, interior_state, ghost_state, child, 1, 1, patch_mass,
+                                                status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm, const double *eta_rest,
+                                const double *wave_tol, uint8_t *cell_bits, int blocks_per_patch,
+                                void *stream) {
+    if (lv.num_patches <= 0) return 0;
+    dim3 grid(blocks_per_patch, lv.num_patches);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_flag_cells<M><<<grid, NTA, 0, st>>>(lv, state, prm, eta_rest, wave_tol, cell_bits);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_version(void) { return 1; }
+
+extern "C" const char *mlamr_build_info(void) {
+    return "mlamr_b200 sm_100a fp64 -fmad=false";
+}

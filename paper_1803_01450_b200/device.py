@@ -1,0 +1,222 @@
+"""Device-resident patch table and level pools.
+
+One :class:`LevelPool` per level holds, in HBM:
+
+* the patch table: int32 boxes [P, 4] and int64 element offsets [P];
+* two state buffers (double buffering for the out-of-place step; the
+  buffer a step read from is the driver's time-interpolation stash), each
+  3M planes of ``field_stride`` float64 -- h_0..h_{M-1}, hu_*, hv_* -- with
+  every patch a (ny+4) x (nx+4) row-major block (mesh.py:181-186) starting
+  at a 256-byte aligned offset;
+* one bathymetry plane of the same shape;
+* int32 owner maps over the level's index space (+2-cell frame): interior
+  owner (last in list order wins) and, for levels that act as parents,
+  frame owner (first in list order wins) -- the gather precedence of
+  ghost.py:29-86;
+* the step work list: 16x32 interior tiles (patch, j0, i0).
+
+PyTorch is used only as the allocator and stream provider; every kernel
+is in ``libmlamr_b200.so`` (no CPU fallback).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .mesh import GHOST_WIDTH, LevelSpec
+
+ALIGN = 32          # elements: patch blocks start on 256-byte boundaries
+TILE_Y, TILE_X = 16, 32
+NTHREADS = 256
+
+
+def _stream_handle(stream: torch.cuda.Stream) -> int:
+    return stream.cuda_stream
+
+
+def tile_list(boxes: np.ndarray) -> np.ndarray:
+    """(patch, j0, i0) for every 16x32 interior tile, patch-major."""
+    if len(boxes) == 0:
+        return np.zeros((0, 3), np.int32)
+    nx = boxes[:, 2] - boxes[:, 0] + 1
+    ny = boxes[:, 3] - boxes[:, 1] + 1
+    tx = (nx + TILE_X - 1) // TILE_X
+    ty = (ny + TILE_Y - 1) // TILE_Y
+    cnt = tx * ty
+    p = np.repeat(np.arange(len(boxes)), cnt)
+    start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
+    k = np.arange(cnt.sum()) - np.repeat(start, cnt)
+    txr = np.repeat(tx, cnt)
+    j0 = (k // txr) * TILE_Y
+    i0 = (k % txr) * TILE_X
+    return np.stack([p, j0, i0], axis=1).astype(np.int32)
+
+
+class LevelPool:
+    """All patches of one level, resident on the device."""
+
+    def __init__(self, spec: LevelSpec, boxes, M: int, device: torch.device,
+                 stream: torch.cuda.Stream, need_gown: bool):
+        self.spec = spec
+        self.M = M
+        self.device = device
+        self.stream = stream
+        b = np.asarray(boxes, dtype=np.int64).reshape(-1, 4)
+        self.boxes = b
+        self.P = len(b)
+        nx = b[:, 2] - b[:, 0] + 1
+        ny = b[:, 3] - b[:, 1] + 1
+        self.ncells = int((nx * ny).sum())
+        size = (nx + 2 * GHOST_WIDTH) * (ny + 2 * GHOST_WIDTH)
+        aligned = (size + ALIGN - 1) // ALIGN * ALIGN
+        self.offsets = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.int64) if self.P else \
+            np.zeros(0, np.int64)
+        self.FS = max(int(aligned.sum()), ALIGN)
+        self.max_cells = int(size.max()) if self.P else 0
+        self.max_interior = int((nx * ny).max()) if self.P else 0
+        with torch.cuda.stream(stream):
+            self.buf = [torch.zeros(3 * M * self.FS, dtype=torch.float64, device=device),
+                        torch.zeros(3 * M * self.FS, dtype=torch.float64, device=device)]
+            self.bathy = torch.zeros(self.FS, dtype=torch.float64, device=device)
+            self.box_d = torch.from_numpy(b.astype(np.int32)).to(device, non_blocking=False)
+            self.off_d = torch.from_numpy(self.offsets).to(device)
+            tl = tile_list(b)
+            self.tiles = tl
+            self.n_tiles = len(tl)
+            self.tiles_d = torch.from_numpy(tl).to(device) if len(tl) else torch.zeros(3, dtype=torch.int32, device=device)
+            self.tile_acc = torch.zeros(max(self.n_tiles, 1) * (M + 2), dtype=torch.float64, device=device)
+            self.speed_bits = torch.full((max(self.P, 1),), -1, dtype=torch.int64, device=device)
+            mapn = (spec.nx + 2 * GHOST_WIDTH) * (spec.ny + 2 * GHOST_WIDTH)
+            self.own = torch.full((mapn,), -1, dtype=torch.int32, device=device)
+            self.gown = torch.full((mapn,), -1, dtype=torch.int32, device=device) if need_gown else None
+        self.child: Optional[torch.Tensor] = None   # finer level's coarsened owner map
+        self.cur = 0
+        self.ghosts_in_cur = False
+        self.time = 0.0
+        L = N.lib()
+        sh = _stream_handle(stream)
+        if self.P:
+            N.check(L.mlamr_paint_owner(self.own.data_ptr(), spec.nx, spec.ny, self.box_d.data_ptr(),
+                                        self.P, 0, 0, 1, 1, self.max_interior, sh), "paint own")
+            if self.gown is not None:
+                N.check(L.mlamr_paint_owner(self.gown.data_ptr(), spec.nx, spec.ny, self.box_d.data_ptr(),
+                                            self.P, GHOST_WIDTH, 1, 1, 1, self.max_cells, sh), "paint gown")
+
+    # -- views ---------------------------------------------------------------
+    @property
+    def state(self) -> torch.Tensor:
+        return self.buf[self.cur]
+
+    @property
+    def other(self) -> torch.Tensor:
+        return self.buf[1 - self.cur]
+
+    def struct(self, state: Optional[torch.Tensor] = None) -> N.Level:
+        s = self.spec
+        lv = N.Level()
+        lv.num_patches = self.P
+        lv.num_layers = self.M
+        lv.level_nx = s.nx
+        lv.level_ny = s.ny
+        lv.dx = s.dx
+        lv.dy = s.dy
+        lv.field_stride = self.FS
+        lv.box = self.box_d.data_ptr()
+        lv.offset = self.off_d.data_ptr()
+        lv.state = (self.state if state is None else state).data_ptr()
+        lv.bathy = self.bathy.data_ptr()
+        lv.own = self.own.data_ptr()
+        lv.gown = self.gown.data_ptr() if self.gown is not None else None
+        return lv
+
+    def blocks_per_patch(self, cells: int) -> int:
+        return int(max(1, min(64, (cells + NTHREADS - 1) // NTHREADS)))
+
+    # -- host transfer (frames, flags, tests) ----------------------------------
+    def patch_arrays(self, p: int, which: Optional[torch.Tensor] = None, host: Optional[np.ndarray] = None):
+        """(h, hu, hv, bathy) numpy arrays [M, NY, NX] of patch p."""
+        lo_i, lo_j, hi_i, hi_j = self.boxes[p]
+        NX = hi_i - lo_i + 1 + 2 * GHOST_WIDTH
+        NY = hi_j - lo_j + 1 + 2 * GHOST_WIDTH
+        off = int(self.offsets[p])
+        if host is None:
+            host = self.download(which)
+        st, bathy = host
+        M = self.M
+        blk = st[:, off:off + NX * NY].reshape(3 * M, NY, NX)
+        return (blk[:M].copy(), blk[M:2 * M].copy(), blk[2 * M:].copy(),
+                bathy[off:off + NX * NY].reshape(NY, NX).copy())
+
+    def download(self, which: Optional[torch.Tensor] = None):
+        t = self.state if which is None else which
+        torch.cuda.current_stream().wait_stream(self.stream)
+        st = t.view(3 * self.M, self.FS).cpu().numpy()
+        return st, self.bathy.cpu().numpy()
+
+    def upload_patches(self, arrays, which: Optional[torch.Tensor] = None, bathy: bool = False) -> None:
+        """arrays[p] = (h, hu, hv) [M, NY, NX] (or a bathymetry [NY, NX])."""
+        M = self.M
+        if bathy:
+            host = np.zeros(self.FS)
+        else:
+            host = np.zeros((3 * M, self.FS))
+        for p, arr in enumerate(arrays):
+            off = int(self.offsets[p])
+            if bathy:
+                host[off:off + arr.size] = arr.ravel()
+            else:
+                h, hu, hv = arr
+                n = h[0].size
+                for m in range(M):
+                    host[m, off:off + n] = h[m].ravel()
+                    host[M + m, off:off + n] = hu[m].ravel()
+                    host[2 * M + m, off:off + n] = hv[m].ravel()
+        t = torch.from_numpy(host.reshape(-1))
+        with torch.cuda.stream(self.stream):
+            if bathy:
+                self.bathy.copy_(t)
+            else:
+                (self.state if which is None else which).copy_(t)
+
+
+def empty_level_struct(spec: LevelSpec, M: int) -> N.Level:
+    """A level with no patches (owner maps NULL: every lookup misses)."""
+    lv = N.Level()
+    lv.num_patches = 0
+    lv.num_layers = M
+    lv.level_nx = spec.nx
+    lv.level_ny = spec.ny
+    lv.dx = spec.dx
+    lv.dy = spec.dy
+    lv.field_stride = 0
+    lv.box = None
+    lv.offset = None
+    lv.state = None
+    lv.bathy = None
+    lv.own = None
+    lv.gown = None
+    return lv
+
+
+def paint_child_map(parent_spec: LevelSpec, fine_boxes: np.ndarray, rx: int, ry: int,
+                    device, stream) -> torch.Tensor:
+    """Owner map, in the parent's index space, of the fine boxes' coarse
+    footprints (coverage_mask, mesh.py:271-279)."""
+    mapn = (parent_spec.nx + 2 * GHOST_WIDTH) * (parent_spec.ny + 2 * GHOST_WIDTH)
+    with torch.cuda.stream(stream):
+        m = torch.full((mapn,), -1, dtype=torch.int32, device=device)
+        if len(fine_boxes):
+            bd = torch.from_numpy(np.asarray(fine_boxes, np.int32).reshape(-1, 4)).to(device)
+            nx = fine_boxes[:, 2] - fine_boxes[:, 0] + 1
+            ny = fine_boxes[:, 3] - fine_boxes[:, 1] + 1
+            mc = int(((nx // rx) * (ny // ry)).max())
+            N.check(N.lib().mlamr_paint_owner(m.data_ptr(), parent_spec.nx, parent_spec.ny, bd.data_ptr(),
+                                              len(fine_boxes), 0, 0, rx, ry, mc, stream.cuda_stream),
+                    "paint child")
+            m._keep = bd  # keep the box tensor alive until the stream passes
+    return m

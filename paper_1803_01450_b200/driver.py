@@ -1,0 +1,426 @@
+"""Subcycled multi-level driver on the device (driver.py:89-362 under
+/root/reference/pkg/src/mlamr).
+
+The recursion, host scalars (dt, theta, r_t, times) and flag clustering
+stay in Python exactly as the reference orders them; every per-patch loop
+of the reference is replaced by one level-batched kernel launch through the
+C-ABI:
+
+========================================  =====================================
+reference                                 here
+========================================  =====================================
+``_step_patches`` -> ``step_patch`` xP    ``mlamr_step`` + ``mlamr_step_finalize``
+``fill_level_ghosts`` -> ``fill_ghosts``  ``mlamr_fill_ghosts``
+stash copies (driver.py:260-264)          the step's untouched source buffer
+``average_down``                          ``mlamr_average_down``
+``rebuild_child_level`` data movement     ``mlamr_regrid_fill`` / ``_derefine_delta``
+``flag_cells`` per-cell tests             ``mlamr_flag_cells``
+``stable_dt`` / dynamic r_t speeds        ``mlamr_max_speed_tiles``
+``composite_mass`` + ``_check_finite``    ``mlamr_level_reduce``
+========================================  =====================================
+
+Host/device synchronisation happens once per coarse step (dt, status,
+composite mass) plus once per regrid (flag map).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .device import LevelPool, empty_level_struct, paint_child_map
+from .errors import CflViolationError, NumericalAbortError, TimeSyncError, raise_status
+from .mesh import GHOST_WIDTH, IndexBox, LevelSpec, boxes_array, paint
+from .regrid import chop, cluster_flags, nesting_allowed, reference_flags
+from .problems import gradient_flags_map
+
+_TIME_RTOL = 1e-12
+
+
+@dataclass
+class RunStats:
+    """Counters of one run (driver.py:44-86)."""
+    total_cell_updates: int = 0
+    cell_updates_per_level: dict = field(default_factory=dict)
+    num_coarse_steps: int = 0
+    num_regrids: int = 0
+    hyperbolicity_warnings: int = 0
+    wet_prefix_repairs: int = 0
+    clipped_mass: list = field(default_factory=list)
+    refine_delta: list = field(default_factory=list)
+    derefine_delta: list = field(default_factory=list)
+    sync_delta: list = field(default_factory=list)
+    initial_mass: list = field(default_factory=list)
+    final_mass: list = field(default_factory=list)
+
+
+class Simulation:
+    """Device-resident counterpart of driver.Simulation over a harness problem
+    (:mod:`paper_1803_01450_b200.problems`)."""
+
+    def __init__(self, problem, device: str = "cuda", stream: torch.cuda.Stream | None = None):
+        self.lib = N.lib()
+        self.pb = problem
+        self.M = M = problem.num_layers
+        self.prm = N.make_params(M, problem.densities, problem.gravity, problem.dry_tolerance)
+        self.specs = [LevelSpec(*s) for s in problem.level_specs()]
+        self.L = len(self.specs)
+        self.bcs = N.bc_array(problem.boundaries)
+        self.dev = torch.device(device)
+        self.stream = stream or torch.cuda.current_stream(self.dev)
+        self.sh = self.stream.cuda_stream
+        with torch.cuda.stream(self.stream):
+            self.status = torch.zeros(1, dtype=torch.int32, device=self.dev)
+            self.bad = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=self.dev)
+            self.acc = torch.zeros(M + 2, dtype=torch.float64, device=self.dev)
+            self.delta_acc = torch.zeros(3, M, dtype=torch.float64, device=self.dev)  # refine, derefine, event
+            self.level_bathy = [torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(self.dev)
+                                for b in problem.bathy_levels]
+            self.scratch = torch.zeros(1, dtype=torch.float64, device=self.dev)
+        self.levels: dict[int, LevelPool] = {}
+        self.steps = {s.level: 0 for s in self.specs}
+        self._stash = {}
+        self.stats = RunStats()
+        self.time = 0.0
+        self.launches = 0
+
+        base = self._new_pool(1, boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)]))
+        self._set_initial(base)
+        self.levels[1] = base
+        for lev in range(1, self.L):
+            self._rebuild(lev, init=True)
+        self._mass_prev = self.composite_mass()
+        self.stats.initial_mass = list(self._mass_prev)
+
+    # -- helpers ----------------------------------------------------------------
+    def spec(self, level: int) -> LevelSpec:
+        return self.specs[level - 1]
+
+    def _call(self, fn, *args, what=""):
+        self.launches += 1
+        N.check(fn(*args), what or fn.__name__)
+
+    def _new_pool(self, level: int, boxes: np.ndarray) -> LevelPool:
+        pool = LevelPool(self.spec(level), boxes, self.M, self.dev, self.stream, need_gown=level < self.L)
+        if pool.P:
+            self._call(self.lib.mlamr_fill_bathymetry, pool.struct(), self.level_bathy[level - 1].data_ptr(),
+                       self.bcs, self.sh)
+        return pool
+
+    def _set_initial(self, pool: LevelPool) -> None:
+        arrays = []
+        for b in pool.boxes:
+            box = IndexBox(*map(int, b)).grown(GHOST_WIDTH)
+            arrays.append(self.pb.initial_state_box(pool.spec.level, tuple(box)))
+        pool.upload_patches(arrays)
+
+    def _sync_status(self, where: str = "") -> None:
+        st = int(self.status.item())
+        if st:
+            bad = int(self.bad.item())
+            if st & N.ST_CFL:
+                raise CflViolationError(f"Courant number > 1 on patch {bad} {where}")
+            raise_status(st, where)
+
+    # -- mass accounting and finite check (driver.py:138-153, 286-297) ---------
+    def _level_reduce(self, level: int) -> torch.Tensor:
+        pool = self.levels[level]
+        if pool.P == 0:
+            return torch.zeros(self.M, dtype=torch.float64, device=self.dev)
+        bpp = pool.blocks_per_patch(pool.max_cells)
+        with torch.cuda.stream(self.stream):
+            part = torch.empty(pool.P * bpp * self.M, dtype=torch.float64, device=self.dev)
+            ghosts = pool.state if pool.ghosts_in_cur else pool.other
+            child = pool.child.data_ptr() if pool.child is not None else None
+            self._call(self.lib.mlamr_level_reduce, pool.struct(), pool.state.data_ptr(), ghosts.data_ptr(),
+                       child, part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
+            s = self.spec(level)
+            return part.view(-1, self.M).sum(dim=0) * (s.dx * s.dy)
+
+    def composite_mass(self) -> np.ndarray:
+        with torch.cuda.stream(self.stream):
+            tot = torch.zeros(self.M, dtype=torch.float64, device=self.dev)
+            for lev in range(1, self.L + 1):
+                if lev in self.levels:
+                    tot = tot + self._level_reduce(lev)
+        self.stream.synchronize()
+        return tot.cpu().numpy()
+
+    # -- ghost filling (driver.py:157-190) ------------------------------------
+    def fill_level_ghosts(self, level: int, t: float) -> None:
+        pool = self.levels[level]
+        if pool.P == 0:
+            return
+        if level == 1:
+            par_ptr, old_ptr, theta, rx, ry = None, None, 0.0, 1, 1
+        else:
+            par = self.levels[level - 1]
+            ps = self.spec(level - 1)
+            rx, ry = ps.r_x, ps.r_y
+            par_struct = par.struct()
+            par_ptr = ctypes.byref(par_struct)
+            old_ptr, theta = None, 0.0
+            st = self._stash.get(level - 1)
+            if st is not None:
+                t0, dt, old = st
+                theta = min(1.0, max(0.0, (t - t0) / dt)) if dt > 0 else 1.0
+                old_ptr = old.data_ptr()
+        self._call(self.lib.mlamr_fill_ghosts, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
+                   self.prm, self.status.data_ptr(), self.sh)
+        pool.ghosts_in_cur = True
+
+    # -- regridding (driver.py:192-222, regrid.py:235-353) -------------------------
+    def level_surfaces(self, level: int, layers) -> tuple:
+        """Level-wide surfaces of the given layers and the covered mask (host)."""
+        pool = self.levels[level]
+        s = self.spec(level)
+        eta = np.zeros((len(layers), s.ny, s.nx))
+        covered = np.zeros((s.ny, s.nx), bool)
+        host = pool.download()
+        g = GHOST_WIDTH
+        for p in range(pool.P):
+            h, hu, hv, b = pool.patch_arrays(p, host=host)
+            hi = h[:, g:-g, g:-g]
+            e = np.cumsum(hi[::-1], axis=0)[::-1] + b[g:-g, g:-g]
+            lo_i, lo_j, hi_i, hi_j = pool.boxes[p]
+            eta[:, lo_j:hi_j + 1, lo_i:hi_i + 1] = e[list(layers)]
+            covered[lo_j:hi_j + 1, lo_i:hi_i + 1] = True
+        return eta, covered
+
+    def flags_for(self, level: int) -> np.ndarray:
+        pool = self.levels[level]
+        s = self.spec(level)
+        rule = self.pb.flag_rule
+        if rule[0] == "reference":
+            with torch.cuda.stream(self.stream):
+                bits = torch.zeros(s.ny * s.nx, dtype=torch.uint8, device=self.dev)
+                er = torch.tensor(list(self.pb.eta_rest), dtype=torch.float64, device=self.dev)
+                wt = torch.tensor(list(self.pb.wave_tolerance), dtype=torch.float64, device=self.dev)
+                self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
+                           er.data_ptr(), wt.data_ptr(), bits.data_ptr(),
+                           pool.blocks_per_patch(pool.max_interior), self.sh)
+            self.stream.synchronize()
+            return reference_flags(bits.cpu().numpy().reshape(s.ny, s.nx), self.M, self.pb.buffer_width)
+        covered = paint(pool.boxes, s.ny, s.nx)
+        if rule[0] == "gradient":
+            from .mesh import dilate
+            eta, covered = self.level_surfaces(level, rule[3])
+            f = gradient_flags_map(eta, covered, s.dx, s.dy, rule[1])
+            return dilate(f, rule[2]) & covered
+        if rule[0] == "bernoulli":
+            from .mesh import dilate
+            f = self.pb.bernoulli_flags(level, self.steps[level])
+            return dilate(f, rule[2]) & covered
+        raise ValueError(rule)
+
+    def _rebuild(self, level: int, init: bool = False) -> bool:
+        s = self.spec(level)
+        rx, ry = s.r_x, s.r_y
+        par = self.levels[level]
+        old = self.levels.get(level + 1)
+        fixed = self.pb.fixed_layout(level + 1) if init else None
+        if fixed is not None:
+            cboxes = sorted([IndexBox(*b).coarsened(rx, ry) for b in fixed], key=lambda b: (b.lo_j, b.lo_i))
+        else:
+            flags = self.flags_for(level)
+            allowed = nesting_allowed(par.boxes, s.ny, s.nx)
+            flags &= allowed
+            cboxes = cluster_flags(flags, self.pb.efficiency_target, allowed)
+            if self.pb.max_patch is not None:
+                cboxes = chop(cboxes, *self.pb.max_patch)
+        nboxes = boxes_array([b.refined(rx, ry) for b in cboxes])
+        if old is not None:
+            key = lambda r: (r[1], r[0])
+            if sorted(map(tuple, nboxes.tolist()), key=key) == sorted(map(tuple, old.boxes.tolist()), key=key):
+                return False
+        elif len(nboxes) == 0:
+            return False
+        new = self._new_pool(level + 1, nboxes)
+        new.time = par.time
+        M = self.M
+        with torch.cuda.stream(self.stream):
+            if init and fixed is None and self.pb.init_mode == "scenario":
+                self._set_initial(new)
+            elif new.P:
+                bpp = new.blocks_per_patch(new.max_interior // (rx * ry))
+                part = torch.zeros(new.P * bpp * M, dtype=torch.float64, device=self.dev)
+                fs = self.spec(level + 1)
+                ol = old.struct() if old is not None else empty_level_struct(fs, M)
+                self._call(self.lib.mlamr_regrid_fill, new.struct(), ol, par.struct(), rx, ry, self.prm,
+                           part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
+                if not init:
+                    self.delta_acc[0] += part.view(-1, M).sum(dim=0)
+            new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
+            if old is not None and old.P and not init:
+                bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
+                part = torch.zeros(old.P * bpp * M, dtype=torch.float64, device=self.dev)
+                self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
+                           rx, ry, self.prm, part.data_ptr(), bpp, self.sh)
+                self.delta_acc[1] += part.view(-1, M).sum(dim=0)
+        new.ghosts_in_cur = False
+        self.levels[level + 1] = new
+        par.child = new_child
+        if level + 2 in self.levels:
+            fs = self.spec(level + 1)
+            new.child = paint_child_map(fs, self.levels[level + 2].boxes, fs.r_x, fs.r_y, self.dev, self.stream)
+        if not init:
+            self.stats.num_regrids += 1
+        # keep the old pool alive until the stream has consumed it
+        self._retired = old
+        return True
+
+    def regrid_from(self, level: int) -> None:
+        if self._rebuild(level):
+            for deeper in range(level + 1, self.L):
+                self._rebuild(deeper)
+
+    # -- stepping (driver.py:224-309) ------------------------------------------------
+    def _step_patches(self, level: int, dt: float) -> None:
+        pool = self.levels[level]
+        if pool.P == 0:
+            return
+        y_first = int(self.steps[level] % 2)
+        with torch.cuda.stream(self.stream):
+            pool.speed_bits.fill_(-1)
+        src, dst = pool.state, pool.other
+        lv = pool.struct(src)
+        self._call(self.lib.mlamr_step, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
+                   pool.n_tiles, dt, y_first, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
+                   self.status.data_ptr(), self.sh)
+        self._call(self.lib.mlamr_step_finalize, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
+                   pool.n_tiles, dt, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
+                   self.acc.data_ptr(), self.status.data_ptr(), self.bad.data_ptr(), self.sh)
+        pool.cur = 1 - pool.cur
+        pool.ghosts_in_cur = False
+        self.stats.total_cell_updates += pool.ncells
+        self.stats.cell_updates_per_level[level] = self.stats.cell_updates_per_level.get(level, 0) + pool.ncells
+
+    def _average_down(self, level: int) -> None:
+        fine = self.levels.get(level + 1)
+        coarse = self.levels[level]
+        if fine is None or fine.P == 0 or coarse.P == 0:
+            return
+        if abs(fine.time - coarse.time) > _TIME_RTOL * max(1.0, abs(coarse.time)):
+            raise TimeSyncError(f"level {level + 1} at t={fine.time!r} vs level {level} at t={coarse.time!r}")
+        s = self.spec(level)
+        bpp = fine.blocks_per_patch(fine.max_interior // (s.r_x * s.r_y))
+        with torch.cuda.stream(self.stream):
+            part = torch.empty(fine.P * bpp * self.M, dtype=torch.float64, device=self.dev)
+        self._call(self.lib.mlamr_average_down, fine.struct(), coarse.struct(), s.r_x, s.r_y, self.prm,
+                   part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
+        self._part_keep = part
+
+    def advance_level(self, level: int, dt: float, t0: float) -> None:
+        if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:
+            self.regrid_from(level)
+        self.fill_level_ghosts(level, t0)
+        pool = self.levels[level]
+        child = self.levels.get(level + 1)
+        has_child = child is not None and child.P > 0
+        self._step_patches(level, dt)
+        self.steps[level] += 1
+        t1 = t0 + dt
+        pool.time = t1
+        if has_child:
+            self.fill_level_ghosts(level, t1)
+            self._stash[level] = (t0, dt, pool.other)
+            s = self.spec(level)
+            dtf = dt / s.r_t
+            for k in range(s.r_t):
+                self.advance_level(level + 1, dtf, t0 + k * dtf)
+            self.levels[level + 1].time = t1
+            self._average_down(level)
+            del self._stash[level]
+
+    # -- coarse step (driver.py:299-362) ----------------------------------------------
+    def level_speed(self, level: int) -> float:
+        pool = self.levels.get(level)
+        if pool is None or pool.P == 0:
+            return 0.0
+        with torch.cuda.stream(self.stream):
+            pool.speed_bits.fill_(-1)
+        self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(), pool.tiles_d.data_ptr(),
+                   pool.n_tiles, self.prm, pool.speed_bits.data_ptr(), self.sh)
+        self.stream.synchronize()
+        bits = pool.speed_bits[:pool.P].cpu().numpy()
+        sp = np.where(bits < 0, 0, bits).view(np.float64)
+        return sp
+
+    def choose_dt(self) -> float:
+        """min over level-1 patches of physics.stable_dt (driver.py:337-339)."""
+        dt = self.pb.dt_max
+        sp = self.level_speed(1)
+        s = self.spec(1)
+        for v in sp:
+            v = float(v)
+            d = self.pb.dt_max if v <= 0.0 else min(self.pb.dt_max, self.pb.cfl * min(s.dx, s.dy) / v)
+            dt = min(dt, d)
+        return dt
+
+    def apply_dynamic_rt(self, dt: float) -> None:
+        if not self.pb.dynamic_rt:
+            return
+        dtl = dt
+        for lev in range(1, self.L):
+            s = self.spec(lev)
+            fs = self.spec(lev + 1)
+            sp = self.level_speed(lev + 1)
+            vmax = 0.0
+            for v in sp:
+                vmax = max(vmax, float(v))
+            rt = self.pb.pick_rt(vmax, dtl, min(fs.dx, fs.dy), max(s.r_x, s.r_y))
+            self.specs[lev - 1] = replace(s, r_t=rt)
+            dtl = dtl / rt
+
+    def advance_coarse_step(self, dt: float) -> None:
+        with torch.cuda.stream(self.stream):
+            self.delta_acc[2].zero_()
+            before = self.delta_acc[:2].sum(dim=0).clone()
+        self.advance_level(1, dt, self.time)
+        self.time += dt
+        self._sync_status(f"at t={self.time:.6g}")
+        mass = self.composite_mass()
+        event = (self.delta_acc[:2].sum(dim=0) - before).cpu().numpy()
+        sync = mass - self._mass_prev - event
+        if not self.stats.sync_delta:
+            self.stats.sync_delta = [0.0] * self.M
+        for m in range(self.M):
+            self.stats.sync_delta[m] += float(sync[m])
+        self._mass_prev = mass
+        self.stats.num_coarse_steps += 1
+        self._sync_status(f"at t={self.time:.6g}")
+
+    def run(self, n_coarse: int) -> RunStats:
+        for _ in range(n_coarse):
+            dt = self.choose_dt()
+            self.apply_dynamic_rt(dt)
+            self.advance_coarse_step(dt)
+        return self.finish()
+
+    def finish(self) -> RunStats:
+        self.stream.synchronize()
+        acc = self.acc.cpu().numpy()
+        M = self.M
+        self.stats.clipped_mass = list(acc[:M])
+        self.stats.hyperbolicity_warnings = int(round(acc[M]))
+        self.stats.wet_prefix_repairs = int(round(acc[M + 1]))
+        d = self.delta_acc.cpu().numpy()
+        self.stats.refine_delta = list(d[0])
+        self.stats.derefine_delta = list(d[1])
+        self.stats.final_mass = list(self._mass_prev)
+        return self.stats
+
+    # -- host views (tests, frames) ------------------------------------------------------
+    def patch_fields(self, level: int):
+        """List of (box, h, hu, hv, bathy) host arrays for every patch of a level."""
+        pool = self.levels[level]
+        host = pool.download()
+        out = []
+        for p in range(pool.P):
+            h, hu, hv, b = pool.patch_arrays(p, host=host)
+            out.append((tuple(int(v) for v in pool.boxes[p]), h, hu, hv, b))
+        return out

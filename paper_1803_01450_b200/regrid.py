@@ -1,0 +1,63 @@
+"""Host-side regrid rules (regrid.py:58-232 under /root/reference/pkg/src/mlamr).
+
+Per-cell flag tests run on the device (``mlamr_flag_cells``); the
+level-wide morphology (dilate/erode, mesh.py:116-141), the nesting mask
+(regrid.nesting_allowed, regrid.py:185-211) and the recursive-bisection
+clustering (regrid.cluster_flags, regrid.py:129-182; native C++ in
+``csrc/host_cluster.cpp``) run on the host, as in the reference.  The
+harness rules of SURVEY.md App. B (gradient and Bernoulli flags, the
+max-patch chop) are here too.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native as N
+from .mesh import IndexBox, dilate, erode, paint
+
+
+def cluster_flags(flags: np.ndarray, efficiency_target: float, allowed=None):
+    """regrid.cluster_flags (regrid.py:129-182) in native C++."""
+    f = np.ascontiguousarray(flags, dtype=np.uint8)
+    ny, nx = f.shape
+    a = None if allowed is None else np.ascontiguousarray(allowed, dtype=np.uint8)
+    cap = max(16, int(f.sum()) + 1)
+    out = np.zeros((cap, 4), dtype=np.int32)
+    n = N.lib().mlamr_cluster_flags(f.ctypes.data, ny, nx, float(efficiency_target),
+                                    None if a is None else a.ctypes.data, out.ctypes.data, cap)
+    if n == -2:
+        raise ValueError("flags outside the allowed region; clear them first")
+    if n < 0:
+        raise RuntimeError("cluster_flags overflow")
+    return [IndexBox(*map(int, r)) for r in out[:n]]
+
+
+def chop(boxes, max_nx: int, max_ny: int):
+    """Harness max-patch-size chop: row-major tiles of at
+    most max_nx x max_ny coarse cells per box, re-sorted by (lo_j, lo_i)."""
+    out = []
+    for b in boxes:
+        for j in range(b.lo_j, b.hi_j + 1, max_ny):
+            for i in range(b.lo_i, b.hi_i + 1, max_nx):
+                out.append(IndexBox(i, j, min(i + max_nx - 1, b.hi_i), min(j + max_ny - 1, b.hi_j)))
+    return sorted(out, key=lambda b: (b.lo_j, b.lo_i))
+
+
+def nesting_allowed(level_boxes: np.ndarray, ny: int, nx: int) -> np.ndarray:
+    """Union of the level's patches eroded by one cell, boundary-exempt."""
+    return erode(paint(level_boxes, ny, nx), 1)
+
+
+def reference_flags(bits: np.ndarray, M: int, buffer_width: int) -> np.ndarray:
+    """regrid.flag_cells (regrid.py:58-101) from the device's per-cell bits:
+    amplitude flags, plus wet cells within ``buffer_width`` of a dry cell of
+    the same layer, dilated by ``buffer_width``, restricted to covered cells."""
+    covered = (bits & 0x80) != 0
+    flags = (bits & 1) != 0
+    for m in range(M):
+        wet = (bits & (2 << m)) != 0
+        flags |= wet & dilate(covered & ~wet, buffer_width)
+    return dilate(flags, buffer_width) & covered
