@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""Benchmark: multilayer AMR cell-layer updates/s (regrid + ghost fill +
+patch step + coarsen) on the BASELINE configuration C4, plus the step
+kernel's fraction of the B200 HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config C4] [--no-e2e] [--no-cpu-baseline]
+
+A "step" is one coarse AMR step: level-1 dt reduction, regrid when due,
+the subcycled ghost fills / patch steps of all levels and the coarsenings
+(driver.py:299-309 of the reference).  The reference arm (``--impl
+reference``) times the oracle port of the reference's CPU algorithm
+(oracle/, C + numpy, all host threads) on a bounded sample of the same
+workload.  Multi-GPU (torchrun, N>1): each rank advances its own replica
+of the workload (weak scaling, no data-path collective yet) and the
+timed region is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "multilayer AMR cell-layer updates/s (regrid + patch step), % of HBM roofline"
+UNIT = "cell-layer updates/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if len(s) > 3 + k and s[3 + k].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def coarse_step(sim):
+    dt = sim.choose_dt()
+    sim.apply_dynamic_rt(dt)
+    sim.advance_coarse_step(dt)
+
+
+def step_bytes(pool, M):
+    """Algorithmic HBM bytes of one step launch on a level:
+    8*[(3M+1)*(nx+2)(ny+2) + 3M*nx*ny] per patch."""
+    b = pool.boxes
+    nx = b[:, 2] - b[:, 0] + 1
+    ny = b[:, 3] - b[:, 1] + 1
+    return int((8 * ((3 * M + 1) * (nx + 2) * (ny + 2) + 3 * M * nx * ny)).sum())
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the oracle port of the reference's CPU algorithm
+# ---------------------------------------------------------------------------
+def cpu_sample_problem(name: str, scale_nx0: int):
+    from paper_1803_01450_b200 import problems
+    if name == "C4":
+        return problems.config4(nx0=scale_nx0), f"C4 generator at L1 {scale_nx0}x{scale_nx0} " \
+                                                f"(dx as C4, {scale_nx0 ** 2 / 512 ** 2:.4f} of C4's area)"
+    return problems.CONFIGS[name](), name
+
+
+def run_cpu(name: str, steps: int, warmup: int, workers: int, scale_nx0: int):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import mlamr_oracle
+    mlamr_oracle.build()
+    pb, desc = cpu_sample_problem(name, scale_nx0)
+    sim = mlamr_oracle.Simulation(pb, workers=workers)
+    for _ in range(warmup):
+        coarse_step(sim)
+    c0 = sim.stats.total_cell_updates
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        coarse_step(sim)
+    t = time.perf_counter() - t0
+    cells = (sim.stats.total_cell_updates - c0) * pb.num_layers
+    return cells / t, t, desc, sim
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    workers = os.cpu_count() or 1
+    steps = max(1, args.steps)
+    nx0 = 128 if steps + args.warmup <= 8 else 64
+    v, t, desc, sim = run_cpu(args.config, steps, args.warmup, workers, nx0)
+    sample = f"{desc}; {steps} coarse steps after {args.warmup} warm-up; oracle/ C+numpy port, " \
+             f"{workers} threads"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.config} (bounded CPU sample)", "sample": desc},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+def b200_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1803_01450_b200 import _native as N
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    pb = problems.CONFIGS[args.config]()
+    M = pb.num_layers
+    stream = torch.cuda.Stream()
+    sim = Simulation(pb, stream=stream)
+    L = sim.L
+    for _ in range(args.warmup):
+        coarse_step(sim)
+
+    # ---- timed region: K coarse steps, device clock ----------------------
+    sim.step_timer_level = L
+    sim.step_events = []
+    launches0 = N.LAUNCHES[0]
+    cells0 = sim.stats.total_cell_updates
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            coarse_step(sim)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    cells = (sim.stats.total_cell_updates - cells0) * M
+    launches = N.LAUNCHES[0] - launches0
+    t_max = ms
+    cells_all = cells
+    if world > 1:
+        tt = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt.item())
+        cc = torch.tensor([cells], dtype=torch.float64, device="cuda")
+        dist.all_reduce(cc, op=dist.ReduceOp.SUM)
+        cells_all = float(cc.item())
+    value = cells_all / (t_max * 1e-3)
+
+    # ---- roofline of the dominant kernel (finest-level step) --------------
+    durs, byts = [], []
+    for a, b, pool in sim.step_events:
+        durs.append(a.elapsed_time(b) * 1e-3)
+        byts.append(step_bytes(pool, M))
+    peak, peak_kind = _peaks()
+    achieved = (sum(byts) / sum(durs)) / 1e9 if durs else None
+    step_share = sum(durs) / (ms * 1e-3) if durs else None
+    sim.step_timer_level = None
+    finest = sim.levels[L]
+
+    # ---- e2e: host buffers -> device -> K steps -> host ---------------------
+    e2e = None
+    if not args.no_e2e:
+        snap = sim.snapshot()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        sim2 = Simulation.restore(pb, snap, stream=stream)
+        c0 = sim2.stats.total_cell_updates
+        for _ in range(args.steps):
+            coarse_step(sim2)
+        out = sim2.snapshot()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        if world > 1:
+            tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt.item())
+        ce = (sim2.stats.total_cell_updates - c0) * M * world
+        e2e = {"value": ce / te, "unit": UNIT,
+               "h2d_bytes_per_step": int(sim2.h2d_bytes / args.steps),
+               "d2h_bytes_per_step": int(sim2.d2h_bytes / args.steps),
+               "timed": "restore(host pinned state -> HBM) + K coarse steps + snapshot(HBM -> host)"}
+        del sim2, snap, out
+
+    # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        workers = os.cpu_count() or 1
+        v, t, desc, _ = run_cpu(args.config, 1, 0, workers, 128)
+        cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
+               "sample": f"{desc}; 1 coarse step (all levels), oracle/ C+numpy port, {t:.1f} s"}
+
+    if rank == 0:
+        pool_bytes = sum(p.state.numel() * 8 * 2 + p.bathy.numel() * 8 for p in sim.levels.values())
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {pb.num_levels} levels, M={M}, "
+                                   f"L1 {pb.coarse_nx}x{pb.coarse_ny}, ratios {pb.ratios_x}",
+                       "patches_per_level": {str(k): v.P for k, v in sim.levels.items()},
+                       "cells_per_level": {str(k): v.ncells for k, v in sim.levels.items()},
+                       "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+                       "l2": (f"inputs larger than L2 (device state {pool_bytes / 1e9:.2f} GB)" if pool_bytes > 126e6 else f"device state {pool_bytes / 1e9:.3f} GB fits in L2 (no flush)"),
+                       "dt_policy": "reference: level-1 stable_dt, r_t subcycling"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "kernel": "mlamr_step (k_step) on the finest level",
+                         "bytes_per_launch": int(np.mean(byts)) if byts else None,
+                         "avg_launch_ms": 1e3 * float(np.mean(durs)) if durs else None,
+                         "share_of_step": step_share, "peak_source": peak_kind},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        b200_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -171,6 +171,20 @@ int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm,
                      const double *eta_rest, const double *wave_tol,
                      uint8_t *cell_bits, int blocks_per_patch, void *stream);
 
+/* Self-test: counts quotients where the shared-reciprocal division used by
+ * the kernels differs bitwise from div.rn.f64 (`bad`, must stay 0) and how
+ * often its fast path declined (`slow`). */
+int mlamr_selftest_div(const double *a, const double *b, int n, unsigned long long *bad,
+                       unsigned long long *slow, void *stream);
+
+/* Host-side (no GPU) recursive-bisection clustering of a flag map
+ * (regrid.cluster_flags, regrid.py:129-182).  flags/allowed are HOST uint8
+ * [ny][nx] (allowed may be NULL); writes (lo_i, lo_j, hi_i, hi_j) boxes
+ * sorted by (lo_j, lo_i) into h_out_boxes.  Returns the box count, -1 if
+ * more than max_boxes, -2 if a flag lies outside `allowed`. */
+int mlamr_cluster_flags(const uint8_t *h_flags, int ny, int nx, double efficiency_target,
+                        const uint8_t *h_allowed, int32_t *h_out_boxes, int max_boxes);
+
 #ifdef __cplusplus
 }
 #endif

@@ -659,15 +659,28 @@ def cluster_flags(flags: np.ndarray, eff: float, allowed: Optional[np.ndarray] =
     return sorted(boxes, key=lambda b: (b.lo_j, b.lo_i))
 
 
-def chop_boxes(boxes, max_nx: int, max_ny: int):
+def chop_boxes(boxes, max_nx: int, max_ny: int, aligned: bool = False):
     """Harness max-patch-size chop: each box is cut into
-    row-major tiles of at most max_nx x max_ny coarse cells, then the list
-    is re-sorted like cluster_flags' output."""
+    tiles of at most max_nx x max_ny coarse cells (from the box corner, or
+    at global multiples of the tile size when ``aligned``), then the list is
+    re-sorted like cluster_flags' output."""
     out = []
     for b in boxes:
-        for j in range(b.lo_j, b.hi_j + 1, max_ny):
-            for i in range(b.lo_i, b.hi_i + 1, max_nx):
-                out.append(Box(i, j, min(i + max_nx - 1, b.hi_i), min(j + max_ny - 1, b.hi_j)))
+        ys = []
+        j = b.lo_j
+        while j <= b.hi_j:
+            nj = ((j // max_ny) + 1) * max_ny if aligned else j + max_ny
+            ys.append((j, min(nj - 1, b.hi_j)))
+            j = nj
+        xs = []
+        i = b.lo_i
+        while i <= b.hi_i:
+            ni = ((i // max_nx) + 1) * max_nx if aligned else i + max_nx
+            xs.append((i, min(ni - 1, b.hi_i)))
+            i = ni
+        for (j0, j1) in ys:
+            for (i0, i1) in xs:
+                out.append(Box(i0, j0, i1, j1))
     return sorted(out, key=lambda b: (b.lo_j, b.lo_i))
 
 
@@ -741,8 +754,13 @@ class Simulation:
     parameters.
     """
 
-    def __init__(self, problem, check_nesting: bool = False):
+    def __init__(self, problem, check_nesting: bool = False, workers: int = 1):
         self.pb = problem
+        self.workers = max(1, int(workers))
+        self._pool = None
+        if self.workers > 1:
+            from concurrent.futures import ThreadPoolExecutor
+            self._pool = ThreadPoolExecutor(self.workers)
         self.prm = Params(problem.num_layers, tuple(problem.densities), problem.gravity,
                           problem.dry_tolerance)
         self.specs = [Spec(*s) for s in problem.level_specs()]
@@ -865,7 +883,7 @@ class Simulation:
             flags &= allowed
             cboxes = cluster_flags(flags, self.pb.efficiency_target, allowed)
             if self.pb.max_patch is not None:
-                cboxes = chop_boxes(cboxes, *self.pb.max_patch)
+                cboxes = chop_boxes(cboxes, *self.pb.max_patch, aligned=self.pb.chop_aligned)
         nboxes = [b.fine(rx, ry) for b in cboxes]
         key = lambda b: (b.lo_j, b.lo_i)
         if sorted(nboxes, key=key) == sorted((p.box for p in old), key=key):
@@ -938,8 +956,14 @@ class Simulation:
     def _step_patches(self, level: int, dt: float) -> None:
         y_first = bool(self.steps[level] % 2)
         n = 0
-        for p in self.patches[level]:
-            r = step_patch(p, dt, self.prm, y_first=y_first)
+        pats = self.patches[level]
+        # the C step releases the GIL (ctypes), so worker threads run patches
+        # concurrently, like the reference's ThreadPoolExecutor (driver.py:231)
+        if self._pool is not None and len(pats) > 1:
+            results = list(self._pool.map(lambda p: step_patch(p, dt, self.prm, y_first=y_first), pats))
+        else:
+            results = [step_patch(p, dt, self.prm, y_first=y_first) for p in pats]
+        for r in results:
             n += r.cells_updated
             self.stats.hyperbolicity_warnings += r.hyperbolicity_fixes
             self.stats.wet_prefix_repairs += r.wet_prefix_repairs

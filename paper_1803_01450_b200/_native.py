@@ -83,6 +83,7 @@ SIGNATURES = {
                                              c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_level_reduce": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
     "mlamr_flag_cells": (ctypes.c_int, [Level, c_vp, Params, c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
+    "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_cluster_flags": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, c_vp,
                                            c_vp, ctypes.c_int]),
 }
@@ -113,7 +114,12 @@ def lib():
     return L
 
 
+LAUNCHES = [0]
+
+
 def check(rc: int, what: str) -> None:
+    """Every C-ABI compute entry point launches exactly one kernel; count it."""
+    LAUNCHES[0] += 1
     if rc != 0:
         raise NativeLibraryError(f"{what} failed to launch (cuda error {rc})")
 

@@ -643,6 +643,27 @@ extern "C" int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_param
     return (int)cudaGetLastError();
 }
 
+// self-test of the shared-reciprocal division against div.rn.f64
+__global__ void k_selftest_div(const double *a, const double *b, int n, unsigned long long *bad,
+                               unsigned long long *slow) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const double x = a[i], y = b[i];
+        bool ok = true;
+        const double r = recip_nr(y);
+        const double q = div_fast(x, y, r, ok);
+        const double ref = x / y;
+        if (!ok) atomicAdd(slow, 1ull);
+        else if (__double_as_longlong(q) != __double_as_longlong(ref) && !(q != q && ref != ref))
+            atomicAdd(bad, 1ull);
+    }
+}
+
+extern "C" int mlamr_selftest_div(const double *a, const double *b, int n, unsigned long long *bad,
+                                  unsigned long long *slow, void *stream) {
+    k_selftest_div<<<592, 256, 0, as_stream(stream)>>>(a, b, n, bad, slow);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int mlamr_version(void) { return 1; }
 
 extern "C" const char *mlamr_build_info(void) {

@@ -28,100 +28,212 @@ constexpr int TY = 16;
 constexpr int PX = TX + 2;
 constexpr int PY = TY + 2;
 constexpr int NPAD = PX * PY;
-constexpr int NFLUX = PY * (PX - 1);  // >= PX * (PY - 1)
+constexpr int NFLUX = PY * PX;  // interface (r,c) stored at the cell index of its left/lower cell
 constexpr int NT = 256;
 
 template <int M>
 struct StepSmem {
-    double S[3 * M + 1][NPAD];  // h_0..h_{M-1}, hu_.., hv_.., B
-    double cw[NPAD];
+    double S[3 * M + 1][NPAD];           // h_0..h_{M-1}, hu_.., hv_.., B
+    double cw[NPAD];                     // sqrt(g * max(sum h, 0))
     double eb[M > 1 ? M - 1 : 1][NPAD];  // eta_{m+1} = B + h_{M-1} + ... + h_{m+1}
-    double src[M > 1 ? M : 1][NPAD];
-    double u[NPAD];
-    double v[NPAD];
-    double vel[NPAD];
-    double F[5][NFLUX];  // Fh, Fm, Fv, hsL, hsR of one layer
+    double u[M][NPAD];                   // normal velocity per layer
+    double v[M][NPAD];                   // transverse velocity per layer
+    double F[2 * M][NFLUX];              // (Fh, Fm) per layer at interface (r,c)-(r,c)+step
+    double src[M > 1 ? M - 1 : 1][NPAD]; // coupling sources of layers 1..M-1
     double red[NT];
     long long redi[NT];
     unsigned char cowet[NPAD];
     unsigned char wetcol[NPAD];
 };
 
-template <int DIR>
-__device__ __forceinline__ int cidx(int o, int a) {
-    return DIR == 0 ? o * PX + a : a * PX + o;
+// All shared-memory phases iterate a rectangle [r0,r1) x [c0,c1) of the
+// padded tile in row-major order with the compile-time row pitch PX, so the
+// index split is a multiply-shift (runtime integer division costs three XU
+// ops and saturated the XU pipe in the first profile) and consecutive
+// threads touch consecutive doubles (no bank conflicts in either sweep
+// direction).
+#define FOR_RECT(r0, r1, c0, c1, ...)                                    \
+    for (int idx_ = threadIdx.x; idx_ < ((r1) - (r0)) * PX; idx_ += NT) { \
+        const int r = (r0) + idx_ / PX;                                  \
+        const int c = idx_ - (idx_ / PX) * PX;                           \
+        if (c < (c0) || c >= (c1)) continue;                             \
+        __VA_ARGS__                                                      \
+    }
+
+// Reconstruction bottoms of layer m at a cell (physics.py:200-207, 105-110):
+// co-wet pairs use Zc (0 for upper layers, B for the bottom layer), others
+// Zf (= Bhat: eta_{m+1} for upper layers, B for the bottom layer).
+template <int M>
+__device__ __forceinline__ double zc_of(const StepSmem<M> &s, int m, int k) {
+    return (m == M - 1) ? s.S[3 * M][k] : 0.0;
 }
-template <int DIR>
-__device__ __forceinline__ int fidx(int o, int a) {
-    return DIR == 0 ? o * (PX - 1) + a : a * PX + o;
+template <int M>
+__device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
+    return (m == M - 1) ? s.S[3 * M][k] : s.eb[m < M - 1 ? m : 0][k];
 }
 
 // One directional sweep of all layers over the staged tile
-// (physics._sweep_x / _sweep_y with _layer_inputs).
-// DIR 0 = x (along columns), 1 = y (along rows).  FIRST: all halo lines
-// (the reference's full=True); else the interior lines only.
+// (physics._sweep_x / _sweep_y with _layer_inputs), three phases:
+//   A  per cell:      layer inputs (cw, cowet, eta_{m+1}) and velocities
+//   B  per interface: HLL fluxes of every layer, coupling sources
+//   C  per cell:      conservative update + pressure correction + source
+// DIR 0 = x (interfaces between columns c, c+1), 1 = y (rows r, r+1).
+// FIRST: all halo lines (the reference's full=True); else interior lines.
 template <int M, int DIR, bool FIRST>
 __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d,
-                           const mlamr_params &prm, const double (&rr)[4][4]) {
-    const int t = threadIdx.x;
-    const int n_along = DIR == 0 ? nx2 : ny2;
-    const int n_outer = DIR == 0 ? ny2 : nx2;
-    const int o0 = FIRST ? 0 : 1;
-    const int o1 = FIRST ? n_outer : n_outer - 1;
-    const int no = o1 - o0;
+                           const mlamr_params &prm, const double (&rr)[4][4], double &best) {
     const double g = prm.gravity;
     const double tol = prm.dry_tolerance;
     const double lam = dt / d;
+    const double yd = recip_nr(d);
     const double *B = s.S[3 * M];
+    constexpr int STEP = DIR == 0 ? 1 : PX;  // neighbour offset along the sweep
+    const int n_along = DIR == 0 ? nx2 : ny2;
+    // lines: DIR 0 sweeps rows (lines = rows), DIR 1 sweeps columns
+    const int lr0 = (DIR == 0 && !FIRST) ? 1 : 0, lr1 = (DIR == 0 && !FIRST) ? ny2 - 1 : ny2;
+    const int lc0 = (DIR == 1 && !FIRST) ? 1 : 0, lc1 = (DIR == 1 && !FIRST) ? nx2 - 1 : nx2;
+    // updated cells exclude the first/last cell along the sweep
+    const int ur0 = DIR == 1 ? 1 : lr0, ur1 = DIR == 1 ? ny2 - 1 : lr1;
+    const int uc0 = DIR == 0 ? 1 : lc0, uc1 = DIR == 0 ? nx2 - 1 : lc1;
+    // interfaces: (r,c)-(r,c+1) for DIR 0, (r,c)-(r+1,c) for DIR 1
+    const int fr1 = DIR == 1 ? ny2 - 1 : lr1;
+    const int fc1 = DIR == 0 ? nx2 - 1 : lc1;
 
-    // Phase D: per-cell layer inputs on the pre-sweep state of this direction.
-    for (int idx = t; idx < no * n_along; idx += NT) {
-        const int o = o0 + idx / n_along;
-        const int a = idx - (idx / n_along) * n_along;
-        const int k = cidx<DIR>(o, a);
+    // ---- Phase A: per-cell inputs on the pre-sweep state of this direction
+    FOR_RECT(lr0, lr1, lc0, lc1, {
+        const int k = r * PX + c;
+        double h[M];
         double hs = 0.0;
+        bool w = true;
 #pragma unroll
-        for (int m = 0; m < M; ++m) hs = hs + s.S[m][k];
-        s.cw[k] = sqrt(g * np_max(hs, 0.0));
-        if (FIRST) s.wetcol[k] = hs > tol;
+        for (int m = 0; m < M; ++m) {
+            h[m] = s.S[m][k];
+            hs = hs + h[m];
+            w = w && (h[m] > tol);
+        }
+        const double cw = sqrt(g * np_max(hs, 0.0));
+        s.cw[k] = cw;
+        s.cowet[k] = (M == 1) ? 1 : w;
         if (M > 1) {
-            bool w = true;
-#pragma unroll
-            for (int m = 0; m < M; ++m) w = w && (s.S[m][k] > tol);
-            s.cowet[k] = w;
             double e = B[k];
 #pragma unroll
             for (int m = M - 1; m >= 1; --m) {
-                e = e + s.S[m][k];
+                e = e + h[m];
                 s.eb[m - 1][k] = e;
             }
-        } else {
-            s.cowet[k] = 1;
         }
-    }
+        const bool interior = FIRST && r >= 1 && r < ny2 - 1 && c >= 1 && c < nx2 - 1 && hs > tol;
+        if (FIRST) s.wetcol[k] = hs > tol;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const bool wet = h[m] > tol;
+            const double hn = s.S[(DIR == 0 ? M : 2 * M) + m][k];
+            const double ht = s.S[(DIR == 0 ? 2 * M : M) + m][k];
+            double u = 0.0, v = 0.0;
+            if (wet) {
+                bool ok = true;
+                const double y = recip_nr(h[m]);
+                u = div_fast(hn, h[m], y, ok);
+                v = div_fast(ht, h[m], y, ok);
+                if (!ok) {
+                    u = hn / h[m];
+                    v = ht / h[m];
+                }
+            }
+            s.u[m][k] = u;
+            s.v[m][k] = v;
+            if (interior) {
+                // observed_max_speed (physics.py:261-278): speed = max(0, x_0,
+                // .., x_{M-1}) + cw with x_m = wet ? max(|hu|/h, |hv|/h) : 0 and
+                // |hu|/h == |hu/h|.  Rounding is monotone, so
+                // max_m(x_m) + cw == max_m(x_m + cw) and 0 + cw == cw: the
+                // running max below is bit-identical to the reference's.
+                const double x = wet ? np_max(fabs(u), fabs(v)) : 0.0;
+                const double cand = (m == 0) ? np_max(cw, x + cw) : x + cw;
+                best = (best < 0.0) ? cand : np_max(best, cand);
+            }
+        }
+    })
     __syncthreads();
 
-    // Phase S: coupling sources on the updated cells (physics.py:208-211).
-    if (M > 1) {
-        const int nu = n_along - 2;
-        for (int idx = t; idx < no * nu; idx += NT) {
-            const int o = o0 + idx / nu;
-            const int a = 1 + idx - (idx / nu) * nu;
-            const int k = cidx<DIR>(o, a);
-            const int km = cidx<DIR>(o, a - 1);
-            const int kp = cidx<DIR>(o, a + 1);
+    // ---- Phase B: HLL fluxes per interface (physics.py:101-161) + sources
+    FOR_RECT(lr0, fr1, lc0, fc1, {
+        const int kl = r * PX + c;
+        const int kr = kl + STEP;
+        const bool cop = s.cowet[kl] && s.cowet[kr];
+        const double cl = s.cw[kl];
+        const double cr = s.cw[kr];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const double hl = s.S[m][kl];
+            const double hr = s.S[m][kr];
+            const double Zl = cop ? zc_of<M>(s, m, kl) : zf_of<M>(s, m, kl);
+            const double Zr = cop ? zc_of<M>(s, m, kr) : zf_of<M>(s, m, kr);
+            const double ul = s.u[m][kl];
+            const double ur = s.u[m][kr];
+            const double Zs = Zl > Zr ? Zl : Zr;
+            double hL = (hl + Zl) - Zs;
+            if (hL < 0.0) hL = 0.0;
+            double hR = (hr + Zr) - Zs;
+            if (hR < 0.0) hR = 0.0;
+            double fh = 0.0, fm = 0.0;
+            if (!(hL <= 0.0 && hR <= 0.0)) {
+                const double sl1 = ul - cl, sl2 = ur - cr;
+                const double SL = sl1 < sl2 ? sl1 : sl2;
+                const double sr1 = ul + cl, sr2 = ur + cr;
+                const double SR = sr1 > sr2 ? sr1 : sr2;
+                const double FLh = hL * ul;
+                const double FRh = hR * ur;
+                const double FLm = ((hL * ul) * ul) + (((0.5 * g) * hL) * hL);
+                const double FRm = ((hR * ur) * ur) + (((0.5 * g) * hR) * hR);
+                if (SL >= 0.0) {
+                    fh = FLh;
+                    fm = FLm;
+                } else if (SR <= 0.0) {
+                    fh = FRh;
+                    fm = FRm;
+                } else {
+                    const double den = SR - SL;
+                    double djump;
+                    if (hL > 0.0 && hR > 0.0)
+                        djump = (hr + zf_of<M>(s, m, kr)) - (hl + zf_of<M>(s, m, kl));
+                    else
+                        djump = hR - hL;
+                    const double nh = ((SR * FLh) - (SL * FRh)) + ((SL * SR) * djump);
+                    const double nm = ((SR * FLm) - (SL * FRm)) + ((SL * SR) * ((hR * ur) - (hL * ul)));
+                    bool ok = true;
+                    const double y = recip_nr(den);
+                    fh = div_fast(nh, den, y, ok);
+                    fm = div_fast(nm, den, y, ok);
+                    if (!ok) {
+                        fh = nh / den;
+                        fm = nm / den;
+                    }
+                }
+            }
+            s.F[2 * m][kl] = fh;
+            s.F[2 * m + 1][kl] = fm;
+        }
+        // coupling sources of layers >= 1 for the interface's upper cell
+        // (physics.py:208-211), on the pre-sweep state
+        const int a = DIR == 0 ? c : r;
+        if (M > 1 && a + 1 < n_along - 1) {
+            const int k = kr, km = kl, kp = kr + STEP;
             const bool wm = s.cowet[km] && s.cowet[k];
             const bool wp = s.cowet[k] && s.cowet[kp];
 #pragma unroll
-            for (int m = 0; m < M; ++m) {
+            for (int m = 1; m < M; ++m) {
                 double acc = 0.0;
                 bool has = false;
+                bool ok = true;
                 if (m < M - 1) {
-                    const double *f = s.eb[m];
+                    const double *f = s.eb[m < M - 1 ? m : 0];
                     const double dm = wm ? f[k] - f[km] : 0.0;
                     const double dp = wp ? f[kp] - f[k] : 0.0;
-                    const double grad = 0.5 * (dp + dm);
-                    acc = (((-g) * s.S[m][k]) * grad) / d;
+                    const double num = ((-g) * s.S[m][k]) * (0.5 * (dp + dm));
+                    double q = div_fast(num, d, yd, ok);
+                    if (!ok) q = num / d;
+                    acc = q;
                     has = true;
                 }
 #pragma unroll
@@ -129,139 +241,69 @@ __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     const double *f = s.S[kk];
                     const double dm = wm ? f[k] - f[km] : 0.0;
                     const double dp = wp ? f[kp] - f[k] : 0.0;
-                    const double grad = 0.5 * (dp + dm);
-                    const double term = ((((-rr[kk][m]) * g) * s.S[m][k]) * grad) / d;
-                    acc = has ? acc + term : term;
+                    const double num = (((-rr[kk][m]) * g) * s.S[m][k]) * (0.5 * (dp + dm));
+                    ok = true;
+                    double q = div_fast(num, d, yd, ok);
+                    if (!ok) q = num / d;
+                    acc = has ? acc + q : q;
                     has = true;
                 }
-                s.src[m][k] = acc;
+                s.src[m - 1][k] = acc;
             }
         }
-    }
-    // (the syncthreads at the top of the layer loop orders Phase S)
+    })
+    __syncthreads();
 
-#pragma unroll 1
-    for (int m = 0; m < M; ++m) {
-        double *H = s.S[m];
-        double *HN = DIR == 0 ? s.S[M + m] : s.S[2 * M + m];
-        double *HT = DIR == 0 ? s.S[2 * M + m] : s.S[M + m];
-        const bool bottom = (m == M - 1);
-        const double *Zf = bottom ? B : s.eb[m < M - 1 ? m : 0];
-        __syncthreads();
-        // Phase U: velocities once per cell (the reference divides twice per
-        // cell, once as a left and once as a right state: same value).
-        for (int idx = t; idx < no * n_along; idx += NT) {
-            const int o = o0 + idx / n_along;
-            const int a = idx - (idx / n_along) * n_along;
-            const int k = cidx<DIR>(o, a);
-            const double h = H[k];
-            const bool wet = h > tol;
-            const double u = wet ? HN[k] / h : 0.0;
-            const double v = wet ? HT[k] / h : 0.0;
-            s.u[k] = u;
-            s.v[k] = v;
-            if (FIRST) {
-                const int r = DIR == 0 ? o : a;
-                const int c = DIR == 0 ? a : o;
-                if (r >= 1 && r < ny2 - 1 && c >= 1 && c < nx2 - 1) {
-                    // observed_max_speed (physics.py:269-276): |hu|/h == |hu/h|
-                    const double x = wet ? np_max(fabs(u), fabs(v)) : 0.0;
-                    s.vel[k] = (m == 0) ? np_max(0.0, x) : np_max(s.vel[k], x);
-                }
-            }
-        }
-        __syncthreads();
-        // Phase F: one HLL flux per interface (physics.py:101-161).
-        const int ni = n_along - 1;
-        for (int idx = t; idx < no * ni; idx += NT) {
-            const int o = o0 + idx / ni;
-            const int a = idx - (idx / ni) * ni;
-            const int kl = cidx<DIR>(o, a);
-            const int kr = cidx<DIR>(o, a + 1);
-            const int fi = fidx<DIR>(o, a);
-            const double hl = H[kl];
-            const double hr = H[kr];
-            double Zl, Zr;
-            if (s.cowet[kl] && s.cowet[kr]) {
-                Zl = bottom ? B[kl] : 0.0;
-                Zr = bottom ? B[kr] : 0.0;
-            } else {
-                Zl = Zf[kl];
-                Zr = Zf[kr];
-            }
-            const double ul = s.u[kl];
-            const double ur = s.u[kr];
-            const double Zs = Zl > Zr ? Zl : Zr;
-            double hL = (hl + Zl) - Zs;
-            if (hL < 0.0) hL = 0.0;
-            double hR = (hr + Zr) - Zs;
-            if (hR < 0.0) hR = 0.0;
-            s.F[3][fi] = hL;
-            s.F[4][fi] = hR;
-            if (hL <= 0.0 && hR <= 0.0) {
-                s.F[0][fi] = 0.0;
-                s.F[1][fi] = 0.0;
-                s.F[2][fi] = 0.0;
-                continue;
-            }
-            const double cl = s.cw[kl];
-            const double cr = s.cw[kr];
-            const double sl1 = ul - cl, sl2 = ur - cr;
-            const double SL = sl1 < sl2 ? sl1 : sl2;
-            const double sr1 = ul + cl, sr2 = ur + cr;
-            const double SR = sr1 > sr2 ? sr1 : sr2;
-            const double FLh = hL * ul;
-            const double FRh = hR * ur;
-            const double FLm = ((hL * ul) * ul) + (((0.5 * g) * hL) * hL);
-            const double FRm = ((hR * ur) * ur) + (((0.5 * g) * hR) * hR);
-            double fh, fm;
-            if (SL >= 0.0) {
-                fh = FLh;
-                fm = FLm;
-            } else if (SR <= 0.0) {
-                fh = FRh;
-                fm = FRm;
-            } else {
-                const double den = SR - SL;
-                double djump;
-                if (hL > 0.0 && hR > 0.0) {
-                    const double Bl = bottom ? B[kl] : Zf[kl];
-                    const double Br = bottom ? B[kr] : Zf[kr];
-                    djump = (hr + Br) - (hl + Bl);
+    // ---- Phase C: conservative update + pressure correction + source
+    FOR_RECT(ur0, ur1, uc0, uc1, {
+        const int k = r * PX + c;
+        const int km = k - STEP, kp = k + STEP;
+        const bool copl = s.cowet[km] && s.cowet[k];
+        const bool copr = s.cowet[k] && s.cowet[kp];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            double *H = s.S[m];
+            double *HN = s.S[(DIR == 0 ? M : 2 * M) + m];
+            double *HT = s.S[(DIR == 0 ? 2 * M : M) + m];
+            const double h0 = H[k];
+            // this cell's reconstructed depths at its two faces: hsR of the
+            // left interface and hsL of the right one (physics.py:113-121)
+            const double Zl_l = copl ? zc_of<M>(s, m, km) : zf_of<M>(s, m, km);
+            const double Zk_l = copl ? zc_of<M>(s, m, k) : zf_of<M>(s, m, k);
+            const double Zk_r = copr ? zc_of<M>(s, m, k) : zf_of<M>(s, m, k);
+            const double Zr_r = copr ? zc_of<M>(s, m, kp) : zf_of<M>(s, m, kp);
+            const double Zs_l = Zl_l > Zk_l ? Zl_l : Zk_l;
+            const double Zs_r = Zk_r > Zr_r ? Zk_r : Zr_r;
+            double hsR_l = (h0 + Zk_l) - Zs_l;
+            if (hsR_l < 0.0) hsR_l = 0.0;
+            double hsL_r = (h0 + Zk_r) - Zs_r;
+            if (hsL_r < 0.0) hsL_r = 0.0;
+            const double fhl = s.F[2 * m][km], fhr = s.F[2 * m][k];
+            const double fml = s.F[2 * m + 1][km], fmr = s.F[2 * m + 1][k];
+            // upwinded transverse flux (physics.py:155-161)
+            const double fvl = fhl > 0.0 ? fhl * s.v[m][km] : (fhl < 0.0 ? fhl * s.v[m][k] : 0.0);
+            const double fvr = fhr > 0.0 ? fhr * s.v[m][k] : (fhr < 0.0 ? fhr * s.v[m][kp] : 0.0);
+            H[k] = h0 - lam * (fhr - fhl);
+            double hn = (HN[k] - lam * (fmr - fml)) - (((lam * 0.5) * g) * ((hsR_l * hsR_l) - (hsL_r * hsL_r)));
+            if (M > 1) {
+                double sm;
+                if (m == 0) {  // physics.py:210, from the pre-sweep eta_1 and own h_0
+                    const double *f = s.eb[0];
+                    const double dm = copl ? f[k] - f[km] : 0.0;
+                    const double dp = copr ? f[kp] - f[k] : 0.0;
+                    const double num = ((-g) * h0) * (0.5 * (dp + dm));
+                    bool ok = true;
+                    sm = div_fast(num, d, yd, ok);
+                    if (!ok) sm = num / d;
                 } else {
-                    djump = hR - hL;
+                    sm = s.src[m - 1][k];
                 }
-                fh = (((SR * FLh) - (SL * FRh)) + ((SL * SR) * djump)) / den;
-                fm = (((SR * FLm) - (SL * FRm)) + ((SL * SR) * ((hR * ur) - (hL * ul)))) / den;
+                hn = hn + dt * sm;
             }
-            s.F[0][fi] = fh;
-            s.F[1][fi] = fm;
-            double fv;
-            if (fh > 0.0)
-                fv = fh * s.v[kl];
-            else if (fh < 0.0)
-                fv = fh * s.v[kr];
-            else
-                fv = 0.0;
-            s.F[2][fi] = fv;
-        }
-        __syncthreads();
-        // Phase C: conservative update + pressure correction (+ source).
-        const int nu = n_along - 2;
-        for (int idx = t; idx < no * nu; idx += NT) {
-            const int o = o0 + idx / nu;
-            const int a = 1 + idx - (idx / nu) * nu;
-            const int k = cidx<DIR>(o, a);
-            const int fl = fidx<DIR>(o, a - 1);
-            const int fr = fidx<DIR>(o, a);
-            H[k] = H[k] - lam * (s.F[0][fr] - s.F[0][fl]);
-            double hn = (HN[k] - lam * (s.F[1][fr] - s.F[1][fl])) -
-                        (((lam * 0.5) * g) * ((s.F[4][fl] * s.F[4][fl]) - (s.F[3][fr] * s.F[3][fr])));
-            if (M > 1) hn = hn + dt * s.src[m][k];
             HN[k] = hn;
-            HT[k] = HT[k] - lam * (s.F[2][fr] - s.F[2][fl]);
+            HT[k] = HT[k] - lam * (fvr - fvl);
         }
-    }
+    })
     __syncthreads();
 }
 
@@ -292,40 +334,32 @@ __global__ void __launch_bounds__(NT) k_step(mlamr_level lv, const double *__res
 #pragma unroll
         for (int b = 0; b < 4; ++b) rr[a][b] = (a < M && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
 
-    // stage the padded tile: 3M state planes + bathymetry
-    const int npad = ny2 * nx2;
+    // stage the padded tile with asynchronous 8-byte copies (LDGSTS): every
+    // thread keeps ~3*(3M+1) global loads in flight instead of serialising
+    // load -> shared store pairs
 #pragma unroll 1
     for (int q = 0; q < 3 * M + 1; ++q) {
         const double *g = (q < 3 * M) ? src + q * FS : lv.bathy;
-        for (int idx = t; idx < npad; idx += NT) {
-            const int r = idx / nx2;
-            const int c = idx - r * nx2;
-            s.S[q][r * PX + c] = __ldg(g + base + (int64_t)r * pv.NX + c);
-        }
+        FOR_RECT(0, ny2, 0, nx2, {
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(&s.S[q][r * PX + c]);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                         "l"(g + base + (int64_t)r * pv.NX + c));
+        })
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+    asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
 
+    double best = -1.0;  // running observed speed over this thread's cells
     if (YFIRST)
-        sweep_tile<M, 1, true>(s, ny2, nx2, dt, lv.dy, prm, rr);
+        sweep_tile<M, 1, true>(s, ny2, nx2, dt, lv.dy, prm, rr, best);
     else
-        sweep_tile<M, 0, true>(s, ny2, nx2, dt, lv.dx, prm, rr);
+        sweep_tile<M, 0, true>(s, ny2, nx2, dt, lv.dx, prm, rr, best);
 
-    // observed max speed of the pre-step interior (vel from the first sweep's
-    // Phase U, cw/wetcol from its Phase D): speed = vel + sqrt(g*max(H,0))
+    // observed max speed of the pre-step interior
     {
-        double best = -1.0;
-        bool any = false;
-        for (int idx = t; idx < ty * tx; idx += NT) {
-            const int r = 1 + idx / tx;
-            const int c = 1 + idx - (idx / tx) * tx;
-            const int k = r * PX + c;
-            if (!s.wetcol[k]) continue;
-            const double sp = s.vel[k] + s.cw[k];
-            best = any ? np_max(best, sp) : sp;
-            any = true;
-        }
         // block max (NaN-propagating); -1 marks "no wet column"
-        s.red[t] = any ? best : -1.0;
+        s.red[t] = best;
         __syncthreads();
         for (int st = NT / 2; st > 0; st >>= 1) {
             if (t < st) {
@@ -343,9 +377,9 @@ __global__ void __launch_bounds__(NT) k_step(mlamr_level lv, const double *__res
     }
 
     if (YFIRST)
-        sweep_tile<M, 0, false>(s, ny2, nx2, dt, lv.dx, prm, rr);
+        sweep_tile<M, 0, false>(s, ny2, nx2, dt, lv.dx, prm, rr, best);
     else
-        sweep_tile<M, 1, false>(s, ny2, nx2, dt, lv.dy, prm, rr);
+        sweep_tile<M, 1, false>(s, ny2, nx2, dt, lv.dy, prm, rr, best);
 
     // post-processing on the tile interior (physics.py:360-376)
     const double tol = prm.dry_tolerance;
@@ -354,9 +388,7 @@ __global__ void __launch_bounds__(NT) k_step(mlamr_level lv, const double *__res
     for (int m = 0; m < M; ++m) negs[m] = 0.0;
     long long fixes = 0, repairs = 0;
     const double coef = prm.gravity * (1.0 - rr[0][1]);
-    for (int idx = t; idx < ty * tx; idx += NT) {
-        const int r = 1 + idx / tx;
-        const int c = 1 + idx - (idx / tx) * tx;
+    FOR_RECT(1, ny2 - 1, 1, nx2 - 1, {
         const int k = r * PX + c;
         double h[M], hu[M], hv[M];
 #pragma unroll
@@ -372,7 +404,16 @@ __global__ void __launch_bounds__(NT) k_step(mlamr_level lv, const double *__res
             const double h1 = h[0], h2 = h[1 % M];
             if (h1 > tol && h2 > tol) {
                 const double hu1 = hu[0], hu2 = hu[1 % M], hv1 = hv[0], hv2 = hv[1 % M];
-                const double u1 = hu1 / h1, u2 = hu2 / h2, v1 = hv1 / h1, v2 = hv2 / h2;
+                bool ok = true;
+                const double y1 = recip_nr(h1), y2 = recip_nr(h2);
+                double u1 = div_fast(hu1, h1, y1, ok), v1 = div_fast(hv1, h1, y1, ok);
+                double u2 = div_fast(hu2, h2, y2, ok), v2 = div_fast(hv2, h2, y2, ok);
+                if (!ok) {
+                    u1 = hu1 / h1;
+                    u2 = hu2 / h2;
+                    v1 = hv1 / h1;
+                    v2 = hv2 / h2;
+                }
                 const double du = u1 - u2, dv = v1 - v2;
                 const double shear2 = (du * du) + (dv * dv);
                 const double bound = coef * (h1 + h2);
@@ -413,7 +454,7 @@ __global__ void __launch_bounds__(NT) k_step(mlamr_level lv, const double *__res
             dst[(M + m) * FS + gaddr] = hu[m];
             dst[(2 * M + m) * FS + gaddr] = hv[m];
         }
-    }
+    })
     // per-tile partials (fixed-order tree sums)
     double *acc = tile_acc + (int64_t)tile * (M + 2);
 #pragma unroll

@@ -62,7 +62,21 @@ class Simulation:
     """Device-resident counterpart of driver.Simulation over a harness problem
     (:mod:`paper_1803_01450_b200.problems`)."""
 
-    def __init__(self, problem, device: str = "cuda", stream: torch.cuda.Stream | None = None):
+    def __init__(self, problem, device: str = "cuda", stream: torch.cuda.Stream | None = None,
+                 _restore: dict | None = None):
+        self._common_init(problem, device, stream)
+        if _restore is not None:
+            self._restore_from(_restore)
+            return
+        base = self._new_pool(1, boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)]))
+        self._set_initial(base)
+        self.levels[1] = base
+        for lev in range(1, self.L):
+            self._rebuild(lev, init=True)
+        self._mass_prev = self.composite_mass()
+        self.stats.initial_mass = list(self._mass_prev)
+
+    def _common_init(self, problem, device, stream) -> None:
         self.lib = N.lib()
         self.pb = problem
         self.M = M = problem.num_layers
@@ -87,14 +101,10 @@ class Simulation:
         self.stats = RunStats()
         self.time = 0.0
         self.launches = 0
-
-        base = self._new_pool(1, boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)]))
-        self._set_initial(base)
-        self.levels[1] = base
-        for lev in range(1, self.L):
-            self._rebuild(lev, init=True)
-        self._mass_prev = self.composite_mass()
-        self.stats.initial_mass = list(self._mass_prev)
+        self.d2h_bytes = 0
+        self.h2d_bytes = 0
+        self.step_timer_level = None   # record CUDA events around this level's step kernel
+        self.step_events = []
 
     # -- helpers ----------------------------------------------------------------
     def spec(self, level: int) -> LevelSpec:
@@ -112,13 +122,26 @@ class Simulation:
         return pool
 
     def _set_initial(self, pool: LevelPool) -> None:
-        arrays = []
-        for b in pool.boxes:
-            box = IndexBox(*map(int, b)).grown(GHOST_WIDTH)
-            arrays.append(self.pb.initial_state_box(pool.spec.level, tuple(box)))
+        """Evaluate the problem's initial condition once per band of patches
+        sharing the same rows (the evaluators are cellwise, so slicing a band
+        equals evaluating each patch box) and upload it."""
+        g = GHOST_WIDTH
+        arrays = [None] * pool.P
+        bands = {}
+        for p, b in enumerate(pool.boxes):
+            bands.setdefault((int(b[1]), int(b[3])), []).append(p)
+        for (lo_j, hi_j), members in bands.items():
+            lo_i = int(min(pool.boxes[p][0] for p in members)) - g
+            hi_i = int(max(pool.boxes[p][2] for p in members)) + g
+            h, hu, hv = self.pb.initial_state_box(pool.spec.level, (lo_i, lo_j - g, hi_i, hi_j + g))
+            for p in members:
+                a = int(pool.boxes[p][0]) - g - lo_i
+                w = int(pool.boxes[p][2] - pool.boxes[p][0]) + 1 + 2 * g
+                arrays[p] = (h[:, :, a:a + w], hu[:, :, a:a + w], hv[:, :, a:a + w])
         pool.upload_patches(arrays)
 
     def _sync_status(self, where: str = "") -> None:
+        self.d2h_bytes += 4
         st = int(self.status.item())
         if st:
             bad = int(self.bad.item())
@@ -148,6 +171,7 @@ class Simulation:
                 if lev in self.levels:
                     tot = tot + self._level_reduce(lev)
         self.stream.synchronize()
+        self.d2h_bytes += 8 * self.M
         return tot.cpu().numpy()
 
     # -- ghost filling (driver.py:157-190) ------------------------------------
@@ -204,6 +228,7 @@ class Simulation:
                            er.data_ptr(), wt.data_ptr(), bits.data_ptr(),
                            pool.blocks_per_patch(pool.max_interior), self.sh)
             self.stream.synchronize()
+            self.d2h_bytes += s.ny * s.nx
             return reference_flags(bits.cpu().numpy().reshape(s.ny, s.nx), self.M, self.pb.buffer_width)
         covered = paint(pool.boxes, s.ny, s.nx)
         if rule[0] == "gradient":
@@ -231,7 +256,7 @@ class Simulation:
             flags &= allowed
             cboxes = cluster_flags(flags, self.pb.efficiency_target, allowed)
             if self.pb.max_patch is not None:
-                cboxes = chop(cboxes, *self.pb.max_patch)
+                cboxes = chop(cboxes, *self.pb.max_patch, aligned=self.pb.chop_aligned)
         nboxes = boxes_array([b.refined(rx, ry) for b in cboxes])
         if old is not None:
             key = lambda r: (r[1], r[0])
@@ -288,9 +313,17 @@ class Simulation:
             pool.speed_bits.fill_(-1)
         src, dst = pool.state, pool.other
         lv = pool.struct(src)
+        timed = self.step_timer_level == level
+        if timed:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.stream)
         self._call(self.lib.mlamr_step, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
                    pool.n_tiles, dt, y_first, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
                    self.status.data_ptr(), self.sh)
+        if timed:
+            e1.record(self.stream)
+            self.step_events.append((e0, e1, pool))
         self._call(self.lib.mlamr_step_finalize, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
                    pool.n_tiles, dt, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
                    self.acc.data_ptr(), self.status.data_ptr(), self.bad.data_ptr(), self.sh)
@@ -346,6 +379,7 @@ class Simulation:
         self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(), pool.tiles_d.data_ptr(),
                    pool.n_tiles, self.prm, pool.speed_bits.data_ptr(), self.sh)
         self.stream.synchronize()
+        self.d2h_bytes += 8 * pool.P
         bits = pool.speed_bits[:pool.P].cpu().numpy()
         sp = np.where(bits < 0, 0, bits).view(np.float64)
         return sp
@@ -385,6 +419,7 @@ class Simulation:
         self._sync_status(f"at t={self.time:.6g}")
         mass = self.composite_mass()
         event = (self.delta_acc[:2].sum(dim=0) - before).cpu().numpy()
+        self.d2h_bytes += 8 * self.M
         sync = mass - self._mass_prev - event
         if not self.stats.sync_delta:
             self.stats.sync_delta = [0.0] * self.M
@@ -413,6 +448,65 @@ class Simulation:
         self.stats.derefine_delta = list(d[1])
         self.stats.final_mass = list(self._mass_prev)
         return self.stats
+
+    # -- checkpoint: host snapshot / restore (pinned host buffers) ----------------------------
+    def snapshot(self) -> dict:
+        """Copy the whole hierarchy (current buffers incl. ghost frames,
+        bathymetry, layouts, clocks and counters) into pinned host memory."""
+        snap = {"time": self.time, "steps": dict(self.steps), "specs": list(self.specs), "levels": {},
+                "acc": None, "delta_acc": None, "mass_prev": np.array(self._mass_prev),
+                "stats": replace(self.stats)}
+        nbytes = 0
+        with torch.cuda.stream(self.stream):
+            for lev, pool in self.levels.items():
+                st = torch.empty(pool.state.shape, dtype=torch.float64, pin_memory=True)
+                st.copy_(pool.state, non_blocking=True)
+                ba = torch.empty(pool.bathy.shape, dtype=torch.float64, pin_memory=True)
+                ba.copy_(pool.bathy, non_blocking=True)
+                nbytes += st.numel() * 8 + ba.numel() * 8
+                snap["levels"][lev] = {"boxes": pool.boxes.copy(), "state": st, "bathy": ba, "time": pool.time,
+                                       "ghosts": pool.ghosts_in_cur}
+            acc = torch.empty(self.acc.shape, dtype=torch.float64, pin_memory=True)
+            acc.copy_(self.acc, non_blocking=True)
+            dacc = torch.empty(self.delta_acc.shape, dtype=torch.float64, pin_memory=True)
+            dacc.copy_(self.delta_acc, non_blocking=True)
+        self.stream.synchronize()
+        snap["acc"], snap["delta_acc"] = acc, dacc
+        snap["nbytes"] = nbytes
+        self.d2h_bytes += nbytes
+        return snap
+
+    @classmethod
+    def restore(cls, problem, snap: dict, device: str = "cuda", stream=None) -> "Simulation":
+        """Rebuild a device hierarchy from :meth:`snapshot` output (host->device)."""
+        return cls(problem, device=device, stream=stream, _restore=snap)
+
+    def _restore_from(self, snap: dict) -> None:
+        self.time = snap["time"]
+        self.steps = dict(snap["steps"])
+        self.specs = list(snap["specs"])
+        self.stats = replace(snap["stats"])
+        nbytes = 0
+        for lev in sorted(snap["levels"]):
+            d = snap["levels"][lev]
+            pool = LevelPool(self.spec(lev), d["boxes"], self.M, self.dev, self.stream, need_gown=lev < self.L)
+            with torch.cuda.stream(self.stream):
+                pool.state.copy_(d["state"], non_blocking=True)
+                pool.bathy.copy_(d["bathy"], non_blocking=True)
+            nbytes += d["state"].numel() * 8 + d["bathy"].numel() * 8
+            pool.time = d["time"]
+            pool.ghosts_in_cur = d["ghosts"]
+            self.levels[lev] = pool
+        for lev in range(1, self.L):
+            if lev + 1 in self.levels:
+                s = self.spec(lev)
+                self.levels[lev].child = paint_child_map(s, self.levels[lev + 1].boxes, s.r_x, s.r_y,
+                                                         self.dev, self.stream)
+        with torch.cuda.stream(self.stream):
+            self.acc.copy_(snap["acc"], non_blocking=True)
+            self.delta_acc.copy_(snap["delta_acc"], non_blocking=True)
+        self._mass_prev = np.array(snap["mass_prev"])
+        self.h2d_bytes += nbytes
 
     # -- host views (tests, frames) ------------------------------------------------------
     def patch_fields(self, level: int):

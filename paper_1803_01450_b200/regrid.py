@@ -35,14 +35,26 @@ def cluster_flags(flags: np.ndarray, efficiency_target: float, allowed=None):
     return [IndexBox(*map(int, r)) for r in out[:n]]
 
 
-def chop(boxes, max_nx: int, max_ny: int):
-    """Harness max-patch-size chop: row-major tiles of at
-    most max_nx x max_ny coarse cells per box, re-sorted by (lo_j, lo_i)."""
+def chop(boxes, max_nx: int, max_ny: int, aligned: bool = False):
+    """Harness max-patch-size chop: each box is cut into
+    tiles of at most max_nx x max_ny coarse cells -- from the box corner, or
+    (``aligned``) at global multiples of the tile size, so that interior
+    tiles of neighbouring boxes line up -- then re-sorted by (lo_j, lo_i)."""
     out = []
     for b in boxes:
-        for j in range(b.lo_j, b.hi_j + 1, max_ny):
-            for i in range(b.lo_i, b.hi_i + 1, max_nx):
-                out.append(IndexBox(i, j, min(i + max_nx - 1, b.hi_i), min(j + max_ny - 1, b.hi_j)))
+        if aligned:
+            js = list(range(b.lo_j - b.lo_j % max_ny + max_ny, b.hi_j + 1, max_ny))
+            is_ = list(range(b.lo_i - b.lo_i % max_nx + max_nx, b.hi_i + 1, max_nx))
+            jcuts = [b.lo_j] + js
+            icuts = [b.lo_i] + is_
+        else:
+            jcuts = list(range(b.lo_j, b.hi_j + 1, max_ny))
+            icuts = list(range(b.lo_i, b.hi_i + 1, max_nx))
+        for a, j in enumerate(jcuts):
+            j1 = (jcuts[a + 1] - 1) if a + 1 < len(jcuts) else b.hi_j
+            for c, i in enumerate(icuts):
+                i1 = (icuts[c + 1] - 1) if c + 1 < len(icuts) else b.hi_i
+                out.append(IndexBox(i, j, i1, j1))
     return sorted(out, key=lambda b: (b.lo_j, b.lo_i))
 
 

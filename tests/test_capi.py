@@ -60,9 +60,10 @@ def test_chop_and_nesting_host_logic(oracle):
     from paper_1803_01450_b200.mesh import IndexBox
     from paper_1803_01450_b200.regrid import chop, nesting_allowed
     boxes = [IndexBox(0, 0, 40, 17), IndexBox(50, 3, 52, 60)]
-    got = [tuple(b) for b in chop(boxes, 16, 8)]
-    ref = [tuple(b) for b in oracle.chop_boxes([oracle.Box(*b) for b in boxes], 16, 8)]
-    assert got == ref
+    for aligned in (False, True):
+        got = [tuple(b) for b in chop(boxes, 16, 8, aligned)]
+        ref = [tuple(b) for b in oracle.chop_boxes([oracle.Box(*b) for b in boxes], 16, 8, aligned)]
+        assert got == ref
     rng = np.random.default_rng(3)
     bx = np.array([[2, 3, 20, 30], [25, 0, 40, 12]])
     m = nesting_allowed(bx, 32, 48)
