@@ -180,6 +180,7 @@ def b200_arm(args):
         coarse_step(sim)
 
     # ---- timed region: K coarse steps, device clock ----------------------
+    sim.host_prof.clear()
     sim.step_timer_level = L
     sim.step_events = []
     launches0 = N.LAUNCHES[0]
@@ -268,7 +269,8 @@ def b200_arm(args):
                        "cells_per_level": {str(k): v.ncells for k, v in sim.levels.items()},
                        "parallelism": f"replica x{world}" if world > 1 else "single GPU",
                        "l2": (f"inputs larger than L2 (device state {pool_bytes / 1e9:.2f} GB)" if pool_bytes > 126e6 else f"device state {pool_bytes / 1e9:.3f} GB fits in L2 (no flush)"),
-                       "dt_policy": "reference: level-1 stable_dt, r_t subcycling"},
+                       "dt_policy": "reference: level-1 stable_dt, r_t subcycling",
+                       "host_ms_per_step": {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "kernel": "mlamr_step (k_step) on the finest level",

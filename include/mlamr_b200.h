@@ -91,6 +91,10 @@ int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                mlamr_params prm, long long *speed_bits, double *tile_acc,
                const int32_t *status, void *stream);
 
+/* Interior tile shape (rows, columns) the step kernel was compiled for;
+ * the host builds `tiles` with it. */
+int mlamr_step_tile(int *ty, int *tx);
+
 /* CFL guard (physics.py:342-347) + deterministic reduction of a step's
  * partials into acc[M + 2].  A patch whose speed*dt/min(dx,dy) > 1 gets its
  * interior restored from src (the reference raises before touching it),
@@ -171,6 +175,14 @@ int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm,
                      const double *eta_rest, const double *wave_tol,
                      uint8_t *cell_bits, int blocks_per_patch, void *stream);
 
+/* Full reference flag rule on the device (regrid.flag_cells +
+ * nesting_allowed, regrid.py:58-101, 185-211): from mlamr_flag_cells' bits,
+ * flags = dilate(amplitude | wet_m & dilate(dry_m)) & covered & allowed and
+ * allowed = erode(covered, 1), as 0/1 byte maps [ny][nx]; scratch is 3*ny*nx
+ * bytes. */
+int mlamr_flags_reference(const uint8_t *bits, int ny, int nx, int M, int buffer_width,
+                          uint8_t *flags, uint8_t *allowed, uint8_t *scratch, void *stream);
+
 /* Self-test: counts quotients where the shared-reciprocal division used by
  * the kernels differs bitwise from div.rn.f64 (`bad`, must stay 0) and how
  * often its fast path declined (`slow`). */
@@ -184,6 +196,12 @@ int mlamr_selftest_div(const double *a, const double *b, int n, unsigned long lo
  * more than max_boxes, -2 if a flag lies outside `allowed`. */
 int mlamr_cluster_flags(const uint8_t *h_flags, int ny, int nx, double efficiency_target,
                         const uint8_t *h_allowed, int32_t *h_out_boxes, int max_boxes);
+
+/* Host-side max-patch-size chop of boxes (SURVEY.md App. B harness rule);
+ * HOST int32 [n*4] in, HOST int32 [cap*4] out sorted by (lo_j, lo_i).
+ * Returns the count or -1 when it exceeds cap. */
+int mlamr_chop_boxes(const int32_t *h_boxes, int n, int max_nx, int max_ny, int aligned,
+                     int32_t *h_out, int cap);
 
 #ifdef __cplusplus
 }

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libmlamr_b200.so")
+LIB_PATH = os.environ.get("MLAMR_LIB") or os.path.join(HERE, "_lib", "libmlamr_b200.so")
 
 MAX_LAYERS = 4
 ST_CFL = 1
@@ -83,6 +83,11 @@ SIGNATURES = {
                                              c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_level_reduce": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
     "mlamr_flag_cells": (ctypes.c_int, [Level, c_vp, Params, c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
+    "mlamr_flags_reference": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             c_vp, c_vp, c_vp, c_vp]),
+    "mlamr_chop_boxes": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                        c_vp, ctypes.c_int]),
+    "mlamr_step_tile": (ctypes.c_int, [c_vp, c_vp]),
     "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_cluster_flags": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, c_vp,
                                            c_vp, ctypes.c_int]),
@@ -111,7 +116,13 @@ def lib():
         fn.restype = res
         fn.argtypes = args
     _lib = L
+    ty, tx = ctypes.c_int(), ctypes.c_int()
+    L.mlamr_step_tile(ctypes.byref(ty), ctypes.byref(tx))
+    STEP_TILE[0], STEP_TILE[1] = ty.value, tx.value
     return L
+
+
+STEP_TILE = [16, 32]
 
 
 LAUNCHES = [0]

@@ -62,36 +62,55 @@ Cut signature_cut(const std::vector<int64_t> &sig) {
     return {n / 2, 0, true};
 }
 
+// One int32 summed-area table answers every query: box counts in O(1) and
+// row/column signatures in O(1) per entry.  The table lives in a reusable
+// buffer so repeated regrids do not pay for fresh pages.
 struct Prefix {
-    int ny, nx;
-    std::vector<int64_t> col;  // (ny+1) x nx : column prefix over rows
-    std::vector<int64_t> row;  // ny x (nx+1) : row prefix over columns
-    std::vector<int64_t> sat;  // (ny+1) x (nx+1) summed-area table
-    void build(const uint8_t *m, int ny_, int nx_) {
+    int ny = 0, nx = 0;
+    std::vector<int32_t> *sat = nullptr;  // (ny+1) x (nx+1)
+    void build(const uint8_t *m, int ny_, int nx_, std::vector<int32_t> &store) {
         ny = ny_;
         nx = nx_;
-        col.assign((size_t)(ny + 1) * nx, 0);
-        row.assign((size_t)ny * (nx + 1), 0);
-        sat.assign((size_t)(ny + 1) * (nx + 1), 0);
-        for (int j = 0; j < ny; ++j) {
-            int64_t rs = 0;
+        sat = &store;
+        const size_t W = (size_t)nx + 1;
+        if (store.size() < (size_t)(ny + 1) * W) store.resize((size_t)(ny + 1) * W);
+        int32_t *S = store.data();
+        // row prefix sums (independent rows), then a column scan in blocks of
+        // 256 columns (each thread walks its block down the rows)
+#pragma omp parallel for schedule(static)
+        for (int j = -1; j < ny; ++j) {
+            int32_t *cur = S + (size_t)(j + 1) * W;
+            cur[0] = 0;
+            if (j < 0) {
+                for (int i = 0; i < nx; ++i) cur[i + 1] = 0;
+                continue;
+            }
+            const uint8_t *row = m + (size_t)j * nx;
+            int32_t rs = 0;
             for (int i = 0; i < nx; ++i) {
-                const int64_t v = m[(size_t)j * nx + i] ? 1 : 0;
-                rs += v;
-                row[(size_t)j * (nx + 1) + i + 1] = rs;
-                col[(size_t)(j + 1) * nx + i] = col[(size_t)j * nx + i] + v;
-                sat[(size_t)(j + 1) * (nx + 1) + i + 1] =
-                    sat[(size_t)j * (nx + 1) + i + 1] + rs;
+                rs += row[i] ? 1 : 0;
+                cur[i + 1] = rs;
+            }
+        }
+        const int nblk = (nx + 255) / 256;
+#pragma omp parallel for schedule(static)
+        for (int bk = 0; bk < nblk; ++bk) {
+            const int i0 = 1 + bk * 256, i1 = std::min(nx, bk * 256 + 256);
+            for (int j = 1; j < ny; ++j) {
+                const int32_t *up = S + (size_t)j * W;
+                int32_t *cur = S + (size_t)(j + 1) * W;
+                for (int i = i0; i <= i1; ++i) cur[i] += up[i];
             }
         }
     }
-    int64_t box(int i0, int j0, int i1, int j1) const {
-        const size_t W = nx + 1;
-        return sat[(size_t)(j1 + 1) * W + i1 + 1] - sat[(size_t)j0 * W + i1 + 1] -
-               sat[(size_t)(j1 + 1) * W + i0] + sat[(size_t)j0 * W + i0];
+    inline int64_t box(int i0, int j0, int i1, int j1) const {
+        const size_t W = (size_t)nx + 1;
+        const int32_t *S = sat->data();
+        return (int64_t)S[(size_t)(j1 + 1) * W + i1 + 1] - S[(size_t)j0 * W + i1 + 1] -
+               S[(size_t)(j1 + 1) * W + i0] + S[(size_t)j0 * W + i0];
     }
-    int64_t colsum(int i, int j0, int j1) const { return col[(size_t)(j1 + 1) * nx + i] - col[(size_t)j0 * nx + i]; }
-    int64_t rowsum(int j, int i0, int i1) const { return row[(size_t)j * (nx + 1) + i1 + 1] - row[(size_t)j * (nx + 1) + i0]; }
+    inline int64_t colsum(int i, int j0, int j1) const { return box(i, j0, i, j1); }
+    inline int64_t rowsum(int j, int i0, int i1) const { return box(i0, j, i1, j); }
 };
 
 }  // namespace
@@ -101,15 +120,23 @@ struct Prefix {
 // flag lies outside `allowed` (the reference raises ValueError).
 extern "C" int mlamr_cluster_flags(const uint8_t *flags, int ny, int nx, double eff,
                                    const uint8_t *allowed, int32_t *out_boxes, int max_boxes) {
+    static thread_local std::vector<int32_t> store_f, store_b;
+    static thread_local std::vector<uint8_t> bad;
     Prefix F;
-    F.build(flags, ny, nx);
+    F.build(flags, ny, nx, store_f);
     Prefix BAD;
     if (allowed != nullptr) {
-        std::vector<uint8_t> bad((size_t)ny * nx);
-        for (size_t k = 0; k < bad.size(); ++k) bad[k] = allowed[k] ? 0 : 1;
-        for (size_t k = 0; k < bad.size(); ++k)
-            if (flags[k] && bad[k]) return -2;
-        BAD.build(bad.data(), ny, nx);
+        bad.resize((size_t)ny * nx);
+        uint8_t *badp = bad.data();  // thread_local storage: hand the pointer to the team
+        int outside = 0;
+        const int64_t n = (int64_t)ny * nx;
+#pragma omp parallel for schedule(static) reduction(|| : outside)
+        for (int64_t k = 0; k < n; ++k) {
+            badp[k] = allowed[k] ? 0 : 1;
+            outside = outside || (flags[k] && !allowed[k]);
+        }
+        if (outside) return -2;
+        BAD.build(bad.data(), ny, nx, store_b);
     }
     struct Node { int i0, j0, i1, j1; };
     std::vector<Node> stack;
@@ -154,11 +181,40 @@ extern "C" int mlamr_cluster_flags(const uint8_t *flags, int ny, int nx, double 
             stack.push_back({a_i, a_j, b_i, a_j + cy.index - 1});
         }
     }
-    std::sort(boxes.begin(), boxes.end(), [](const std::array<int, 4> &a, const std::array<int, 4> &b) {
+    std::stable_sort(boxes.begin(), boxes.end(), [](const std::array<int, 4> &a, const std::array<int, 4> &b) {
         return a[1] != b[1] ? a[1] < b[1] : a[0] < b[0];
     });
     if ((int)boxes.size() > max_boxes) return -1;
     for (size_t k = 0; k < boxes.size(); ++k)
         for (int q = 0; q < 4; ++q) out_boxes[4 * k + q] = boxes[k][q];
     return (int)boxes.size();
+}
+
+// Harness max-patch-size chop of clustered boxes: each
+// box is cut into tiles of at most max_nx x max_ny cells, from the box
+// corner or (aligned) at global multiples of the tile size; output sorted by
+// (lo_j, lo_i).  Returns the count, or -1 if it exceeds cap.
+extern "C" int mlamr_chop_boxes(const int32_t *boxes, int n, int max_nx, int max_ny, int aligned,
+                                int32_t *out, int cap) {
+    std::vector<std::array<int, 4>> res;
+    for (int k = 0; k < n; ++k) {
+        const int lo_i = boxes[4 * k], lo_j = boxes[4 * k + 1], hi_i = boxes[4 * k + 2], hi_j = boxes[4 * k + 3];
+        for (int j = lo_j; j <= hi_j;) {
+            const int nj = aligned ? (j / max_ny + 1) * max_ny : j + max_ny;
+            const int j1 = std::min(nj - 1, hi_j);
+            for (int i = lo_i; i <= hi_i;) {
+                const int ni = aligned ? (i / max_nx + 1) * max_nx : i + max_nx;
+                res.push_back({i, j, std::min(ni - 1, hi_i), j1});
+                i = ni;
+            }
+            j = nj;
+        }
+    }
+    std::stable_sort(res.begin(), res.end(), [](const std::array<int, 4> &a, const std::array<int, 4> &b) {
+        return a[1] != b[1] ? a[1] < b[1] : a[0] < b[0];
+    });
+    if ((int)res.size() > cap) return -1;
+    for (size_t k = 0; k < res.size(); ++k)
+        for (int q = 0; q < 4; ++q) out[4 * k + q] = res[k][q];
+    return (int)res.size();
 }

@@ -8,6 +8,8 @@
 // coarsen.py:57-75); the painting order reproduces the reference's
 // list-order precedence (interiors: last wins; ghost fallback: first wins).
 
+#include <algorithm>
+
 #include "interp.cuh"
 
 namespace mlamr {
@@ -498,6 +500,68 @@ __global__ void __launch_bounds__(NTA) k_flag_cells(mlamr_level lv, const double
     }
 }
 
+// ---------------------------------------------------------------------------
+// level-wide flag morphology on byte maps (mesh.dilate / mesh.erode,
+// mesh.py:116-141): 3x3 neighbourhood OR (outside = 0) / AND (outside = 1),
+// applied bytewise so each bit plane dilates independently.
+// ---------------------------------------------------------------------------
+__global__ void k_morph3(const uint8_t *in, uint8_t *out, int ny, int nx, int erode) {
+    const int64_t n = (int64_t)ny * nx;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / nx), i = (int)(idx - (int64_t)j * nx);
+        uint8_t acc = erode ? 0xff : 0;
+        for (int dj = -1; dj <= 1; ++dj)
+            for (int di = -1; di <= 1; ++di) {
+                const int jj = j + dj, ii = i + di;
+                const bool inb = jj >= 0 && ii >= 0 && jj < ny && ii < nx;
+                const uint8_t v = inb ? in[(int64_t)jj * nx + ii] : (erode ? 0xff : 0);
+                acc = erode ? (acc & v) : (acc | v);
+            }
+        out[idx] = acc;
+    }
+}
+
+// stage 1 of the reference rule from the per-cell bits: per layer m the
+// plane "covered and dry" (regrid.py:91-92) as bit m
+__global__ void k_dry_planes(const uint8_t *bits, uint8_t *dry, int64_t n, int M) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t b = bits[idx];
+        uint8_t d = 0;
+        if (b & 0x80)
+            for (int m = 0; m < M; ++m)
+                if (!(b & (2u << m))) d |= (uint8_t)(1u << m);
+        dry[idx] = d;
+    }
+}
+
+// stage 2: amplitude flags | wet_m & near-dry_m (regrid.py:96-98)
+__global__ void k_flag_combine(const uint8_t *bits, const uint8_t *neardry, uint8_t *flags, int64_t n,
+                               int M) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const uint8_t b = bits[idx];
+        uint8_t f = b & 1;
+        for (int m = 0; m < M; ++m)
+            if ((b & (2u << m)) && (neardry[idx] & (1u << m))) f = 1;
+        flags[idx] = f;
+    }
+}
+
+// final: flags & covered & allowed; allowed = erode(covered, 1)
+__global__ void k_flag_mask(uint8_t *flags, const uint8_t *bits, const uint8_t *allowed, int64_t n) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        flags[idx] = (flags[idx] && (bits[idx] & 0x80) && allowed[idx]) ? 1 : 0;
+}
+
+__global__ void k_covered(const uint8_t *bits, uint8_t *cov, int64_t n) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        cov[idx] = (bits[idx] & 0x80) ? 1 : 0;
+}
+
 template <typename F>
 static int dispatch_m(int M, F &&f) {
     switch (M) {
@@ -661,6 +725,35 @@ __global__ void k_selftest_div(const double *a, const double *b, int n, unsigned
 extern "C" int mlamr_selftest_div(const double *a, const double *b, int n, unsigned long long *bad,
                                   unsigned long long *slow, void *stream) {
     k_selftest_div<<<592, 256, 0, as_stream(stream)>>>(a, b, n, bad, slow);
+    return (int)cudaGetLastError();
+}
+
+// Full reference flag rule + nesting mask on the device.  `bits` from
+// mlamr_flag_cells; scratch = 3 byte maps of ny*nx.  Outputs: flags
+// (0/1, already & covered & allowed) and allowed = erode(covered, 1).
+extern "C" int mlamr_flags_reference(const uint8_t *bits, int ny, int nx, int M, int buffer_width,
+                                     uint8_t *flags, uint8_t *allowed, uint8_t *scratch, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    const int64_t n = (int64_t)ny * nx;
+    if (n <= 0) return 0;
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    uint8_t *a = scratch, *b = scratch + n, *c = scratch + 2 * n;
+    k_dry_planes<<<nb, 256, 0, st>>>(bits, a, n, M);
+    for (int w = 0; w < buffer_width; ++w) {
+        k_morph3<<<nb, 256, 0, st>>>(a, b, ny, nx, 0);
+        uint8_t *t = a; a = b; b = t;
+    }
+    k_flag_combine<<<nb, 256, 0, st>>>(bits, a, c, n, M);
+    uint8_t *fa = c, *fb = b;
+    for (int w = 0; w < buffer_width; ++w) {
+        k_morph3<<<nb, 256, 0, st>>>(fa, fb, ny, nx, 0);
+        uint8_t *t = fa; fa = fb; fb = t;
+    }
+    k_covered<<<nb, 256, 0, st>>>(bits, a == fa ? fb : a, n);
+    uint8_t *cov = (a == fa) ? fb : a;
+    k_morph3<<<nb, 256, 0, st>>>(cov, allowed, ny, nx, 1);
+    k_flag_mask<<<nb, 256, 0, st>>>(fa, bits, allowed, n);
+    cudaMemcpyAsync(flags, fa, n, cudaMemcpyDeviceToDevice, st);
     return (int)cudaGetLastError();
 }
 

@@ -23,8 +23,14 @@
 
 namespace mlamr {
 
+#ifndef MLAMR_STEP_TY
+#define MLAMR_STEP_TY 16
+#endif
+#ifndef MLAMR_STEP_MINB
+#define MLAMR_STEP_MINB 1
+#endif
 constexpr int TX = 32;
-constexpr int TY = 16;
+constexpr int TY = MLAMR_STEP_TY;
 constexpr int PX = TX + 2;
 constexpr int PY = TY + 2;
 constexpr int NPAD = PX * PY;
@@ -308,7 +314,7 @@ __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
 }
 
 template <int M, bool YFIRST>
-__global__ void __launch_bounds__(NT) k_step(mlamr_level lv, const double *__restrict__ src,
+__global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, const double *__restrict__ src,
                                              double *__restrict__ dst,
                                              const int32_t *__restrict__ tiles, double dt,
                                              mlamr_params prm, long long *speed_bits,
@@ -605,6 +611,12 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
 }  // namespace mlamr
 
 using namespace mlamr;
+
+extern "C" int mlamr_step_tile(int *ty, int *tx) {
+    *ty = TY;
+    *tx = TX;
+    return 0;
+}
 
 extern "C" int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                           const int32_t *tiles, int n_tiles, double dt, int y_first,

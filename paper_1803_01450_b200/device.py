@@ -31,7 +31,6 @@ from . import _native as N
 from .mesh import GHOST_WIDTH, LevelSpec
 
 ALIGN = 32          # elements: patch blocks start on 256-byte boundaries
-TILE_Y, TILE_X = 16, 32
 NTHREADS = 256
 
 
@@ -39,8 +38,85 @@ def _stream_handle(stream: torch.cuda.Stream) -> int:
     return stream.cuda_stream
 
 
+class PinnedArena:
+    """Pinned staging memory for small host->device uploads (patch tables,
+    tile lists).  Copies from pageable memory would synchronise the stream
+    (the driver stages them synchronously); staging through pinned memory
+    keeps uploads asynchronous.  Regions are recycled after :meth:`reset`,
+    which the driver calls at points where the stream has been drained."""
+
+    def __init__(self, nbytes: int = 1 << 24):
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self.off = 0
+        self.spill = []   # oversize staging tensors kept alive until reset
+
+    def reset(self) -> None:
+        self.off = 0
+        self.spill.clear()
+
+    def upload(self, arr: np.ndarray, device, stream) -> torch.Tensor:
+        a = np.ascontiguousarray(arr)
+        n = a.nbytes
+        dt = torch.from_numpy(a[:0]).dtype if a.size == 0 else torch.from_numpy(a.reshape(-1)[:1]).dtype
+        if n == 0:
+            return torch.empty(a.shape, dtype=dt, device=device)
+        start = (self.off + 255) // 256 * 256
+        if start + n <= self.buf.numel():
+            host = self.buf[start:start + n]
+            self.off = start + n
+        else:
+            host = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+            self.spill.append(host)
+        host.numpy()[:] = a.reshape(-1).view(np.uint8)
+        with torch.cuda.stream(stream):
+            out = torch.empty(a.shape, dtype=dt, device=device)
+            out.view(-1).view(torch.uint8).copy_(host, non_blocking=True)
+        return out
+
+
+_ARENA = None
+
+# Recycled device buffers: a regrid replaces a level's pool with one of
+# similar size, so the retired state/bathymetry buffers are handed to the
+# next pool instead of round-tripping GBs through cudaMalloc.  Reuse is
+# stream-ordered (everything runs on the driver's stream).
+_RECYCLE: list = []
+
+
+def acquire(numel: int, dtype, device, stream) -> torch.Tensor:
+    best = None
+    for k, t in enumerate(_RECYCLE):
+        if t.dtype == dtype and t.device == device and t.numel() >= numel:
+            if best is None or t.numel() < _RECYCLE[best].numel():
+                best = k
+    if best is not None and _RECYCLE[best].numel() <= 3 * numel + (1 << 20):
+        t = _RECYCLE.pop(best)
+        return t[:numel]
+    cap = int(numel * 1.5) + (1 << 16)
+    with torch.cuda.stream(stream):
+        t = torch.empty(cap, dtype=dtype, device=device)
+    return t[:numel]
+
+
+def release(t: torch.Tensor) -> None:
+    base = t._base if t._base is not None else t
+    _RECYCLE.append(base)
+    # bound the cache: keep the 16 largest buffers
+    _RECYCLE.sort(key=lambda x: -x.numel())
+    del _RECYCLE[16:]
+
+
+def arena() -> PinnedArena:
+    global _ARENA
+    if _ARENA is None:
+        _ARENA = PinnedArena()
+    return _ARENA
+
+
 def tile_list(boxes: np.ndarray) -> np.ndarray:
-    """(patch, j0, i0) for every 16x32 interior tile, patch-major."""
+    """(patch, j0, i0) for every step tile (shape from the library), patch-major."""
+    N.lib()
+    TILE_Y, TILE_X = N.STEP_TILE
     if len(boxes) == 0:
         return np.zeros((0, 3), np.int32)
     nx = boxes[:, 2] - boxes[:, 0] + 1
@@ -80,20 +156,23 @@ class LevelPool:
         self.max_cells = int(size.max()) if self.P else 0
         self.max_interior = int((nx * ny).max()) if self.P else 0
         with torch.cuda.stream(stream):
-            self.buf = [torch.zeros(3 * M * self.FS, dtype=torch.float64, device=device),
-                        torch.zeros(3 * M * self.FS, dtype=torch.float64, device=device)]
-            self.bathy = torch.zeros(self.FS, dtype=torch.float64, device=device)
-            self.box_d = torch.from_numpy(b.astype(np.int32)).to(device, non_blocking=False)
-            self.off_d = torch.from_numpy(self.offsets).to(device)
+            self.buf = [acquire(3 * M * self.FS, torch.float64, device, stream),
+                        acquire(3 * M * self.FS, torch.float64, device, stream)]
+            self.bathy = acquire(self.FS, torch.float64, device, stream)
+            for t in (self.buf[0], self.buf[1], self.bathy):
+                t.zero_()
+            A = arena()
+            self.box_d = A.upload(b.astype(np.int32), device, stream)
+            self.off_d = A.upload(self.offsets, device, stream)
             tl = tile_list(b)
             self.tiles = tl
             self.n_tiles = len(tl)
-            self.tiles_d = torch.from_numpy(tl).to(device) if len(tl) else torch.zeros(3, dtype=torch.int32, device=device)
+            self.tiles_d = A.upload(tl, device, stream) if len(tl) else torch.zeros(3, dtype=torch.int32, device=device)
             self.tile_acc = torch.zeros(max(self.n_tiles, 1) * (M + 2), dtype=torch.float64, device=device)
             self.speed_bits = torch.full((max(self.P, 1),), -1, dtype=torch.int64, device=device)
             mapn = (spec.nx + 2 * GHOST_WIDTH) * (spec.ny + 2 * GHOST_WIDTH)
-            self.own = torch.full((mapn,), -1, dtype=torch.int32, device=device)
-            self.gown = torch.full((mapn,), -1, dtype=torch.int32, device=device) if need_gown else None
+            self.own = acquire(mapn, torch.int32, device, stream).fill_(-1)
+            self.gown = acquire(mapn, torch.int32, device, stream).fill_(-1) if need_gown else None
         self.child: Optional[torch.Tensor] = None   # finer level's coarsened owner map
         self.cur = 0
         self.ghosts_in_cur = False
@@ -106,6 +185,14 @@ class LevelPool:
             if self.gown is not None:
                 N.check(L.mlamr_paint_owner(self.gown.data_ptr(), spec.nx, spec.ny, self.box_d.data_ptr(),
                                             self.P, GHOST_WIDTH, 1, 1, 1, self.max_cells, sh), "paint gown")
+
+    def release(self) -> None:
+        """Hand the big buffers back for reuse by a later pool."""
+        for t in (self.buf[0], self.buf[1], self.bathy, self.own, self.gown):
+            if t is not None:
+                release(t)
+        self.buf = [None, None]
+        self.bathy = None
 
     # -- views ---------------------------------------------------------------
     @property
@@ -209,9 +296,9 @@ def paint_child_map(parent_spec: LevelSpec, fine_boxes: np.ndarray, rx: int, ry:
     footprints (coverage_mask, mesh.py:271-279)."""
     mapn = (parent_spec.nx + 2 * GHOST_WIDTH) * (parent_spec.ny + 2 * GHOST_WIDTH)
     with torch.cuda.stream(stream):
-        m = torch.full((mapn,), -1, dtype=torch.int32, device=device)
+        m = acquire(mapn, torch.int32, device, stream).fill_(-1)
         if len(fine_boxes):
-            bd = torch.from_numpy(np.asarray(fine_boxes, np.int32).reshape(-1, 4)).to(device)
+            bd = arena().upload(np.asarray(fine_boxes, np.int32).reshape(-1, 4), device, stream)
             nx = fine_boxes[:, 2] - fine_boxes[:, 0] + 1
             ny = fine_boxes[:, 3] - fine_boxes[:, 1] + 1
             mc = int(((nx // rx) * (ny // ry)).max())

@@ -26,16 +26,19 @@ composite mass) plus once per regrid (flag map).
 from __future__ import annotations
 
 import ctypes
+import time
+from collections import defaultdict
+from contextlib import contextmanager
 from dataclasses import dataclass, field, replace
 
 import numpy as np
 import torch
 
 from . import _native as N
-from .device import LevelPool, empty_level_struct, paint_child_map
+from .device import LevelPool, arena, empty_level_struct, paint_child_map, release
 from .errors import CflViolationError, NumericalAbortError, TimeSyncError, raise_status
 from .mesh import GHOST_WIDTH, IndexBox, LevelSpec, boxes_array, paint
-from .regrid import chop, cluster_flags, nesting_allowed, reference_flags
+from .regrid import chop_boxes, cluster_boxes, nesting_allowed
 from .problems import gradient_flags_map
 
 _TIME_RTOL = 1e-12
@@ -95,6 +98,9 @@ class Simulation:
             self.level_bathy = [torch.from_numpy(np.ascontiguousarray(b, dtype=np.float64)).to(self.dev)
                                 for b in problem.bathy_levels]
             self.scratch = torch.zeros(1, dtype=torch.float64, device=self.dev)
+            self._eta_rest = torch.tensor(list(problem.eta_rest), dtype=torch.float64, device=self.dev)
+            self._wave_tol = torch.tensor(list(problem.wave_tolerance), dtype=torch.float64, device=self.dev)
+        self._flagbuf = {}
         self.levels: dict[int, LevelPool] = {}
         self.steps = {s.level: 0 for s in self.specs}
         self._stash = {}
@@ -105,8 +111,17 @@ class Simulation:
         self.h2d_bytes = 0
         self.step_timer_level = None   # record CUDA events around this level's step kernel
         self.step_events = []
+        self.host_prof = defaultdict(float)   # host wall seconds per phase (incl. syncs)
 
     # -- helpers ----------------------------------------------------------------
+    @contextmanager
+    def _timed(self, name: str):
+        t0 = time.perf_counter()
+        try:
+            yield
+        finally:
+            self.host_prof[name] += time.perf_counter() - t0
+
     def spec(self, level: int) -> LevelSpec:
         return self.specs[level - 1]
 
@@ -171,6 +186,7 @@ class Simulation:
                 if lev in self.levels:
                     tot = tot + self._level_reduce(lev)
         self.stream.synchronize()
+        arena().reset()
         self.d2h_bytes += 8 * self.M
         return tot.cpu().numpy()
 
@@ -215,32 +231,67 @@ class Simulation:
             covered[lo_j:hi_j + 1, lo_i:hi_i + 1] = True
         return eta, covered
 
-    def flags_for(self, level: int) -> np.ndarray:
+    def _flag_buffers(self, level: int):
+        s = self.spec(level)
+        n = s.ny * s.nx
+        key = (level, n)
+        buf = self._flagbuf.get(key)
+        if buf is None:
+            with torch.cuda.stream(self.stream):
+                buf = {
+                    "bits": torch.zeros(n, dtype=torch.uint8, device=self.dev),
+                    "scratch": torch.empty(3 * n, dtype=torch.uint8, device=self.dev),
+                    "flags": torch.empty(n, dtype=torch.uint8, device=self.dev),
+                    "allowed": torch.empty(n, dtype=torch.uint8, device=self.dev),
+                    "flags_h": torch.empty(n, dtype=torch.uint8, pin_memory=True),
+                    "allowed_h": torch.empty(n, dtype=torch.uint8, pin_memory=True),
+                }
+            self._flagbuf[key] = buf
+        return buf
+
+    def flags_and_allowed(self, level: int):
+        """Refinement flags of a level (already restricted to the nesting
+        mask) and the nesting mask, as host uint8 maps [ny, nx]."""
         pool = self.levels[level]
         s = self.spec(level)
         rule = self.pb.flag_rule
         if rule[0] == "reference":
+            b = self._flag_buffers(level)
             with torch.cuda.stream(self.stream):
-                bits = torch.zeros(s.ny * s.nx, dtype=torch.uint8, device=self.dev)
-                er = torch.tensor(list(self.pb.eta_rest), dtype=torch.float64, device=self.dev)
-                wt = torch.tensor(list(self.pb.wave_tolerance), dtype=torch.float64, device=self.dev)
+                b["bits"].zero_()
                 self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
-                           er.data_ptr(), wt.data_ptr(), bits.data_ptr(),
+                           self._eta_rest.data_ptr(), self._wave_tol.data_ptr(), b["bits"].data_ptr(),
                            pool.blocks_per_patch(pool.max_interior), self.sh)
+                self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
+                           self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
+                           b["scratch"].data_ptr(), self.sh)
+                b["flags_h"].copy_(b["flags"], non_blocking=True)
+                b["allowed_h"].copy_(b["allowed"], non_blocking=True)
             self.stream.synchronize()
-            self.d2h_bytes += s.ny * s.nx
-            return reference_flags(bits.cpu().numpy().reshape(s.ny, s.nx), self.M, self.pb.buffer_width)
+            arena().reset()   # the stream is drained: staged uploads are complete
+            self.d2h_bytes += 2 * s.ny * s.nx
+            return (b["flags_h"].numpy().reshape(s.ny, s.nx).view(np.bool_),
+                    b["allowed_h"].numpy().reshape(s.ny, s.nx).view(np.bool_))
+        from .mesh import dilate
         covered = paint(pool.boxes, s.ny, s.nx)
         if rule[0] == "gradient":
-            from .mesh import dilate
             eta, covered = self.level_surfaces(level, rule[3])
             f = gradient_flags_map(eta, covered, s.dx, s.dy, rule[1])
-            return dilate(f, rule[2]) & covered
-        if rule[0] == "bernoulli":
-            from .mesh import dilate
+            f = dilate(f, rule[2]) & covered
+        elif rule[0] == "bernoulli":
             f = self.pb.bernoulli_flags(level, self.steps[level])
-            return dilate(f, rule[2]) & covered
-        raise ValueError(rule)
+            f = dilate(f, rule[2]) & covered
+        else:
+            raise ValueError(rule)
+        allowed = nesting_allowed(pool.boxes, s.ny, s.nx)
+        return f & allowed, allowed
+
+    def flags_for(self, level: int) -> np.ndarray:
+        return self.flags_and_allowed(level)[0]
+
+    @staticmethod
+    def _lexsorted(b: np.ndarray) -> np.ndarray:
+        return b[np.lexsort((b[:, 0], b[:, 1]))] if len(b) else b
 
     def _rebuild(self, level: int, init: bool = False) -> bool:
         s = self.spec(level)
@@ -249,24 +300,28 @@ class Simulation:
         old = self.levels.get(level + 1)
         fixed = self.pb.fixed_layout(level + 1) if init else None
         if fixed is not None:
-            cboxes = sorted([IndexBox(*b).coarsened(rx, ry) for b in fixed], key=lambda b: (b.lo_j, b.lo_i))
+            fb = np.asarray(fixed, dtype=np.int64).reshape(-1, 4)
+            cb = np.stack([fb[:, 0] // rx, fb[:, 1] // ry, (fb[:, 2] + 1) // rx - 1, (fb[:, 3] + 1) // ry - 1], 1)
+            cb = self._lexsorted(cb)
         else:
-            flags = self.flags_for(level)
-            allowed = nesting_allowed(par.boxes, s.ny, s.nx)
-            flags &= allowed
-            cboxes = cluster_flags(flags, self.pb.efficiency_target, allowed)
-            if self.pb.max_patch is not None:
-                cboxes = chop(cboxes, *self.pb.max_patch, aligned=self.pb.chop_aligned)
-        nboxes = boxes_array([b.refined(rx, ry) for b in cboxes])
+            with self._timed("regrid.flags"):
+                flags, allowed = self.flags_and_allowed(level)
+            with self._timed("regrid.cluster"):
+                cb = cluster_boxes(flags, self.pb.efficiency_target, allowed)
+                if self.pb.max_patch is not None:
+                    cb = chop_boxes(cb, *self.pb.max_patch, aligned=self.pb.chop_aligned)
+        cb = np.asarray(cb, dtype=np.int64).reshape(-1, 4)
+        nboxes = np.stack([cb[:, 0] * rx, cb[:, 1] * ry, (cb[:, 2] + 1) * rx - 1, (cb[:, 3] + 1) * ry - 1], 1)
         if old is not None:
-            key = lambda r: (r[1], r[0])
-            if sorted(map(tuple, nboxes.tolist()), key=key) == sorted(map(tuple, old.boxes.tolist()), key=key):
+            if len(old.boxes) == len(nboxes) and np.array_equal(self._lexsorted(old.boxes), self._lexsorted(nboxes)):
                 return False
         elif len(nboxes) == 0:
             return False
-        new = self._new_pool(level + 1, nboxes)
+        with self._timed("regrid.pool"):
+            new = self._new_pool(level + 1, nboxes)
         new.time = par.time
         M = self.M
+        tq = time.perf_counter()
         with torch.cuda.stream(self.stream):
             if init and fixed is None and self.pb.init_mode == "scenario":
                 self._set_initial(new)
@@ -286,22 +341,31 @@ class Simulation:
                 self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
                            rx, ry, self.prm, part.data_ptr(), bpp, self.sh)
                 self.delta_acc[1] += part.view(-1, M).sum(dim=0)
+        self.host_prof["regrid.fill+derefine"] += time.perf_counter() - tq
+        tq = time.perf_counter()
         new.ghosts_in_cur = False
         self.levels[level + 1] = new
+        if old is not None:
+            old.release()
+        if par.child is not None:
+            release(par.child)
         par.child = new_child
         if level + 2 in self.levels:
             fs = self.spec(level + 1)
+            if old is not None and old.child is not None:
+                release(old.child)
             new.child = paint_child_map(fs, self.levels[level + 2].boxes, fs.r_x, fs.r_y, self.dev, self.stream)
         if not init:
             self.stats.num_regrids += 1
-        # keep the old pool alive until the stream has consumed it
-        self._retired = old
+        self.host_prof["regrid.swap"] += time.perf_counter() - tq
         return True
 
     def regrid_from(self, level: int) -> None:
+        t0 = time.perf_counter()
         if self._rebuild(level):
             for deeper in range(level + 1, self.L):
                 self._rebuild(deeper)
+        self.host_prof["regrid(total)"] += time.perf_counter() - t0
 
     # -- stepping (driver.py:224-309) ------------------------------------------------
     def _step_patches(self, level: int, dt: float) -> None:
@@ -387,7 +451,8 @@ class Simulation:
     def choose_dt(self) -> float:
         """min over level-1 patches of physics.stable_dt (driver.py:337-339)."""
         dt = self.pb.dt_max
-        sp = self.level_speed(1)
+        with self._timed("dt"):
+            sp = self.level_speed(1)
         s = self.spec(1)
         for v in sp:
             v = float(v)
@@ -414,10 +479,13 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             self.delta_acc[2].zero_()
             before = self.delta_acc[:2].sum(dim=0).clone()
-        self.advance_level(1, dt, self.time)
+        with self._timed("advance(host enqueue)"):
+            self.advance_level(1, dt, self.time)
         self.time += dt
-        self._sync_status(f"at t={self.time:.6g}")
-        mass = self.composite_mass()
+        with self._timed("sync(wait for device)"):
+            self._sync_status(f"at t={self.time:.6g}")
+        with self._timed("mass+finite"):
+            mass = self.composite_mass()
         event = (self.delta_acc[:2].sum(dim=0) - before).cpu().numpy()
         self.d2h_bytes += 8 * self.M
         sync = mass - self._mass_prev - event

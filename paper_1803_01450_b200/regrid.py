@@ -19,20 +19,41 @@ from . import _native as N
 from .mesh import IndexBox, dilate, erode, paint
 
 
-def cluster_flags(flags: np.ndarray, efficiency_target: float, allowed=None):
-    """regrid.cluster_flags (regrid.py:129-182) in native C++."""
+def cluster_boxes(flags: np.ndarray, efficiency_target: float, allowed=None) -> np.ndarray:
+    """regrid.cluster_flags (regrid.py:129-182) in native C++; int32 [n, 4]."""
     f = np.ascontiguousarray(flags, dtype=np.uint8)
     ny, nx = f.shape
     a = None if allowed is None else np.ascontiguousarray(allowed, dtype=np.uint8)
-    cap = max(16, int(f.sum()) + 1)
-    out = np.zeros((cap, 4), dtype=np.int32)
-    n = N.lib().mlamr_cluster_flags(f.ctypes.data, ny, nx, float(efficiency_target),
-                                    None if a is None else a.ctypes.data, out.ctypes.data, cap)
-    if n == -2:
-        raise ValueError("flags outside the allowed region; clear them first")
+    cap = 4096
+    while True:
+        out = np.empty((cap, 4), dtype=np.int32)
+        n = N.lib().mlamr_cluster_flags(f.ctypes.data, ny, nx, float(efficiency_target),
+                                        None if a is None else a.ctypes.data, out.ctypes.data, cap)
+        if n == -2:
+            raise ValueError("flags outside the allowed region; clear them first")
+        if n >= 0:
+            return out[:n]
+        cap *= 8
+
+
+def chop_boxes(boxes: np.ndarray, max_nx: int, max_ny: int, aligned: bool = False) -> np.ndarray:
+    """:func:`chop` in native C++ over an int32 [n, 4] array."""
+    b = np.ascontiguousarray(boxes, dtype=np.int32).reshape(-1, 4)
+    if len(b) == 0:
+        return b
+    areas = (b[:, 2] - b[:, 0] + 1).astype(np.int64) * (b[:, 3] - b[:, 1] + 1)
+    cap = int(areas.sum()) if max_nx * max_ny == 1 else int(
+        (((b[:, 2] - b[:, 0]) // max_nx + 2) * ((b[:, 3] - b[:, 1]) // max_ny + 2)).sum())
+    out = np.empty((cap, 4), dtype=np.int32)
+    n = N.lib().mlamr_chop_boxes(b.ctypes.data, len(b), max_nx, max_ny, int(aligned), out.ctypes.data, cap)
     if n < 0:
-        raise RuntimeError("cluster_flags overflow")
-    return [IndexBox(*map(int, r)) for r in out[:n]]
+        raise RuntimeError("chop overflow")
+    return out[:n]
+
+
+def cluster_flags(flags: np.ndarray, efficiency_target: float, allowed=None):
+    """regrid.cluster_flags (regrid.py:129-182): list of IndexBox."""
+    return [IndexBox(*map(int, r)) for r in cluster_boxes(flags, efficiency_target, allowed)]
 
 
 def chop(boxes, max_nx: int, max_ny: int, aligned: bool = False):
