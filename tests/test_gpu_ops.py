@@ -71,3 +71,68 @@ def test_interpolate_state_matches_reference_bitwise():
         assert same(oh, c("oh")), (k, mismatch(oh, c("oh")))
         assert same(ohu, c("ohu")), k
         assert same(ohv, c("ohv")), k
+
+
+def _shelf_level_patches(z, prefix, lev):
+    from gpu_util import HostPatch
+    nx, ny = (int(v) for v in z[f"L{lev}_spec"][:2])
+    dx, dy = (float(v) for v in z[f"L{lev}_dxdy"])
+    out = []
+    for k, b in enumerate(z[f"{prefix}L{lev}_boxes"]):
+        p = HostPatch(b, dx, dy, z[f"{prefix}L{lev}_p{k}_h"], z[f"{prefix}L{lev}_p{k}_hu"],
+                      z[f"{prefix}L{lev}_p{k}_hv"], z[f"{prefix}L{lev}_p{k}_bathy"], level=lev)
+        p.time = 0.0
+        out.append(p)
+    return out, (0, 0, nx - 1, ny - 1)
+
+
+def test_fill_ghosts_shim_blended_matches_reference():
+    """ghost.fill_ghosts through a time-blended gather provider
+    (driver.py:157-190) on the reference's captured level-3 state."""
+    from paper_1803_01450_b200 import ops
+    z = load_golden("run_shelf_small.npz")
+    fine, lbox = _shelf_level_patches(z, "gf_before_", 3)
+    parents, _ = _shelf_level_patches(z, "gf_before_", 2)
+    stash = {id(p): (z[f"gf_parent_{k}_oh"], z[f"gf_parent_{k}_ohu"], z[f"gf_parent_{k}_ohv"])
+             for k, p in enumerate(parents)}
+    t, t0, dtp = float(z["gf_t"]), float(z["gf_t0"]), float(z["gf_dt"])
+    theta = min(1.0, max(0.0, (t - t0) / dtp))
+    prov = lambda box: ops.gather(parents, box, 2, blend=(theta, stash))
+    bcs = {"left": "outflow", "right": "outflow", "top": "wall", "bottom": "wall"}
+    prm = _Params(2, (0.95, 1.0))
+    for p in fine:
+        ops.fill_ghosts(p, fine, prov, bcs, lbox, 2, 2, prm)
+    for k, p in enumerate(fine):
+        for f in ("h", "hu", "hv"):
+            ref = z[f"gf_after_L3_p{k}_{f}"]
+            assert same(getattr(p, f), ref), (k, f, mismatch(getattr(p, f), ref))
+
+
+def test_average_down_and_refine_shims_match_oracle(oracle):
+    import copy
+    from shelf_problem import shelf_problem
+    from paper_1803_01450_b200 import ops
+    sim = oracle.Simulation(shelf_problem())
+    for _ in range(2):
+        sim.advance_coarse_step(sim.choose_dt())
+    prm = _Params(2, (0.95, 1.0))
+    for lev in (2, 3):
+        fine = sim.patches[lev]
+        coarse_o = copy.deepcopy(sim.patches[lev - 1])
+        coarse_g = copy.deepcopy(sim.patches[lev - 1])
+        d_o = oracle.average_down(fine, coarse_o, 2, 2, sim.prm)
+        d_g = ops.average_down(fine, coarse_g, 2, 2, prm)
+        for a, b in zip(coarse_o, coarse_g):
+            assert same(a.h, b.h) and same(a.hu, b.hu) and same(a.hv, b.hv), lev
+        np.testing.assert_allclose(d_g, d_o, rtol=1e-9, atol=1e-12)
+    # refine a whole level-3 patch from interior-only level-2 data
+    p_o = copy.deepcopy(sim.patches[3][0])
+    p_g = copy.deepcopy(sim.patches[3][0])
+    run = p_o.box.coarse(2, 2).grow(1)
+    c_o = oracle.gather(sim.patches[2], run, 2, include_ghosts=False)
+    c_g = ops.gather(sim.patches[2], tuple(run), 2, include_ghosts=False)
+    assert same(c_o.h, c_g.h) and np.array_equal(c_o.avail, c_g.avail)
+    d_o = oracle.refine_patch(c_o, p_o, 2, 2, sim.prm)
+    d_g = ops.refine_patch(c_g, p_g, 2, 2, prm)
+    assert same(p_o.h, p_g.h) and same(p_o.hu, p_g.hu) and same(p_o.hv, p_g.hv)
+    np.testing.assert_allclose(d_g, d_o, rtol=1e-12, atol=1e-12)
