@@ -43,49 +43,55 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons during the timed region."""
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms by ONE
+    long-running nvidia-smi process (started before CUDA is initialised, so
+    no fork of a large process happens inside the timed region); a reader
+    thread timestamps the lines and :meth:`window` selects those inside the
+    timed region."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int = 0):
-        self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
+        self.lines = []
+        self.proc = None
+        self.t0 = self.t1 = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([x.strip() for x in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), [x.strip() for x in line.split(",")]))
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        self.t0 = time.time()
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        self.t1 = time.time() + 0.25
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
 
     def summary(self):
-        if not self.samples:
+        samples = [v for (t, v) in self.lines if self.t0 is not None and self.t0 <= t <= (self.t1 or t)]
+        if not samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
-        mx = max((float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()), default=None)
+        num = lambda x: x.replace(".", "").isdigit()
+        sm = sorted(float(s[0]) for s in samples if num(s[0]))
+        mx = max((float(s[1]) for s in samples if num(s[1])), default=None)
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for s in self.samples for k in range(4)
+        reasons = sorted({names[k] for s in samples for k in range(4)
                           if len(s) > 3 + k and s[3 + k].lower() == "active"})
         return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(samples)}
 
 
 def coarse_step(sim):
@@ -137,7 +143,9 @@ def reference_arm(args):
         return
     workers = os.cpu_count() or 1
     steps = max(1, args.steps)
-    nx0 = 128 if steps + args.warmup <= 8 else 64
+    # the oracle keeps the reference's O(P^2) patch scans, so the sample is
+    # kept small enough for the whole run to finish in a few minutes
+    nx0 = 64 if steps + args.warmup <= 12 else 32
     v, t, desc, sim = run_cpu(args.config, steps, args.warmup, workers, nx0)
     sample = f"{desc}; {steps} coarse steps after {args.warmup} warm-up; oracle/ C+numpy port, " \
              f"{workers} threads"
@@ -156,6 +164,8 @@ def reference_arm(args):
 # B200 arm
 # ---------------------------------------------------------------------------
 def b200_arm(args):
+    local0 = int(os.environ.get("LOCAL_RANK", "0"))
+    clk = ClockSampler(local0)   # before CUDA initialisation
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -190,12 +200,21 @@ def b200_arm(args):
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
+    prof = None
+    if os.environ.get("MLAMR_CPROFILE"):
+        import cProfile
+        prof = cProfile.Profile()
+        prof.enable()
+    with clk:
         e0.record(stream)
         for _ in range(args.steps):
             coarse_step(sim)
         e1.record(stream)
         torch.cuda.synchronize()
+    if prof is not None:
+        import pstats
+        prof.disable()
+        pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(20)
     if world > 1:
         dist.barrier()
     ms = e0.elapsed_time(e1)
@@ -253,7 +272,7 @@ def b200_arm(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
-        v, t, desc, _ = run_cpu(args.config, 1, 0, workers, 128)
+        v, t, desc, _ = run_cpu(args.config, 1, 0, workers, 64)
         cpu = {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
                "sample": f"{desc}; 1 coarse step (all levels), oracle/ C+numpy port, {t:.1f} s"}
 
@@ -283,6 +302,7 @@ def b200_arm(args):
             "gpu_launches": launches,
         }
         print(json.dumps(line), flush=True)
+    clk.stop()
     if world > 1:
         dist.destroy_process_group()
 
