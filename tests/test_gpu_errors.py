@@ -1,0 +1,101 @@
+"""Failure detection on the GPU path: the reference's error
+semantics through the C-ABI status word."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, same
+from gpu_util import HostPatch
+
+pytestmark = pytest.mark.gpu
+
+
+class _Params:
+    def __init__(self, M, densities, g=1.0, tol=1e-3):
+        self.num_layers = M
+        self.densities = densities
+        self.gravity = g
+        self.dry_tolerance = tol
+
+
+def test_driver_cfl_violation_raises_and_spares_the_patch():
+    """A dt far above the stable one: CflViolationError, and the violating
+    patches keep their pre-step interior (physics.py:342-347)."""
+    from shelf_problem import shelf_problem
+    from paper_1803_01450_b200.driver import Simulation
+    from paper_1803_01450_b200.errors import CflViolationError
+    sim = Simulation(shelf_problem())
+    before = [f[1].copy() for f in sim.patch_fields(1)]
+    dt = 20.0 * sim.choose_dt()
+    with pytest.raises(CflViolationError):
+        sim.advance_coarse_step(dt)
+    after = sim.patch_fields(1)
+    assert same(after[0][1][:, 2:-2, 2:-2], before[0][:, 2:-2, 2:-2])
+
+
+def test_nonfinite_state_aborts():
+    """A NaN injected into a level-2 interior: NumericalAbortError at the end
+    of the coarse step (driver.py:286-297)."""
+    import torch
+    from shelf_problem import shelf_problem
+    from paper_1803_01450_b200.driver import Simulation
+    from paper_1803_01450_b200.errors import NumericalAbortError
+    sim = Simulation(shelf_problem())
+    pool = sim.levels[2]
+    off = int(pool.offsets[0]) + 2 * (int(pool.boxes[0][2] - pool.boxes[0][0]) + 5) + 2
+    pool.state[off] = float("nan")
+    torch.cuda.synchronize()
+    with pytest.raises(NumericalAbortError):
+        sim.advance_coarse_step(sim.choose_dt())
+
+
+def test_average_down_time_sync_error():
+    from paper_1803_01450_b200 import ops
+    from paper_1803_01450_b200.errors import TimeSyncError
+    M = 2
+    z = np.zeros((M, 8, 8))
+    fine = HostPatch((0, 0, 3, 3), 0.5, 0.5, z + 1.0, z, z, np.zeros((8, 8)))
+    coarse = HostPatch((0, 0, 1, 1), 1.0, 1.0, np.zeros((M, 6, 6)) + 1.0, np.zeros((M, 6, 6)),
+                       np.zeros((M, 6, 6)), np.zeros((6, 6)))
+    fine.time, coarse.time = 1.0, 1.5
+    with pytest.raises(TimeSyncError):
+        ops.average_down([fine], [coarse], 2, 2, _Params(M, (0.95, 1.0)))
+    fine.time = 1.5
+    ops.average_down([fine], [coarse], 2, 2, _Params(M, (0.95, 1.0)))
+    assert np.all(coarse.h[:, 2:-2, 2:-2] == 1.0)
+
+
+def test_refine_geometry_errors():
+    from paper_1803_01450_b200 import ops
+    from paper_1803_01450_b200.errors import GeometryError
+    M = 2
+    cd = ops.CoarseData((0, 0, 3, 3), np.ones((M, 4, 4)), np.zeros((M, 4, 4)), np.zeros((M, 4, 4)),
+                        -np.ones((4, 4)), np.ones((4, 4), bool))
+    fine = HostPatch((0, 0, 7, 7), 0.5, 0.5, np.zeros((M, 12, 12)), np.zeros((M, 12, 12)),
+                     np.zeros((M, 12, 12)), -np.ones((12, 12)))
+    prm = _Params(M, (0.95, 1.0))
+    with pytest.raises(GeometryError):           # region outside the patch
+        ops.refine_patch(cd, fine, 2, 2, prm, region=(4, 4, 9, 9))
+    with pytest.raises(GeometryError):           # not ratio-aligned
+        ops.refine_patch(cd, fine, 2, 2, prm, region=(1, 0, 4, 3))
+    cd.avail[1, 1] = False
+    with pytest.raises(GeometryError):           # incomplete coarse data
+        ops.refine_patch(cd, fine, 2, 2, prm, region=(2, 2, 3, 3))
+    with pytest.raises(GeometryError):           # parents outside the footprint
+        ops.interpolate_state(cd, (0, 0, 9, 9), np.zeros((10, 10)), 2, 2, prm)
+
+
+def test_empty_child_level_runs():
+    """Flags that select nothing leave level 2 empty; the run proceeds on
+    level 1 alone, like the reference with no refinement."""
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+    pb = problems.config2(n_coarse_steps=1)
+    pb.fixed_layouts = {}
+    pb.wave_tolerance = (1e9, 1e9)
+    pb.buffer_width = 0
+    pb.max_patch = None
+    sim = Simulation(pb)
+    assert sim.levels.get(2) is None or sim.levels[2].P == 0
+    sim.advance_coarse_step(sim.choose_dt())
+    assert sim.stats.total_cell_updates == 128 * 128
