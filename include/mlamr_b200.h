@@ -119,7 +119,8 @@ int mlamr_max_speed_tiles(mlamr_level lv, const double *state, const int32_t *ti
 int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent,
                       const double *parent_old_state, double theta,
                       int r_x, int r_y, const int32_t *bcs,
-                      mlamr_params prm, const int32_t *status, void *stream);
+                      mlamr_params prm, const int32_t *status,
+                      const int32_t *patch_list, int n_list, void *stream);
 
 /* Patch bathymetry (frame included) from a level-wide array of in-domain
  * values, then ghost.apply_bathymetry_bcs (ghost.py:118-129). */
@@ -140,12 +141,14 @@ int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x, int r_y,
  * include_ghosts=False).  Refine-delta partials [P_new * blocks * M]. */
 int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_level parent,
                       int r_x, int r_y, mlamr_params prm, double *refine_delta,
-                      int blocks_per_patch, int32_t *status, void *stream);
+                      int blocks_per_patch, int32_t *status,
+                      const int32_t *patch_list, int n_list, void *stream);
 /* Derefine delta (regrid.py:329-348); new_child = the new patches'
  * coarsened owner map in the parent's index space. */
 int mlamr_derefine_delta(mlamr_level oldlv, mlamr_level parent, const int32_t *new_child,
                          int r_x, int r_y, mlamr_params prm, double *derefine_delta,
-                         int blocks_per_patch, void *stream);
+                         int blocks_per_patch, const int32_t *patch_list, int n_list,
+                         void *stream);
 
 /* Standalone interpolate_state (refine.py:158-190) over a gathered coarse
  * array [M][cny][cnx] with availability mask; fine outputs [M][fny][fnx]. */
@@ -165,7 +168,8 @@ int mlamr_interpolate_box(int M, const double *ch, const double *chu, const doub
 int mlamr_level_reduce(mlamr_level lv, const double *interior_state,
                        const double *ghost_state, const int32_t *child,
                        double *patch_mass, int blocks_per_patch,
-                       int32_t *status, void *stream);
+                       int32_t *status, const int32_t *patch_list, int n_list,
+                       void *stream);
 
 /* Reference flag rule, per-cell part (regrid.flag_cells, regrid.py:58-101):
  * cell_bits over the level index space (no frame): bit0 amplitude flag
@@ -173,7 +177,17 @@ int mlamr_level_reduce(mlamr_level lv, const double *interior_state,
  * The dilations are applied by the host. */
 int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm,
                      const double *eta_rest, const double *wave_tol,
-                     uint8_t *cell_bits, int blocks_per_patch, void *stream);
+                     uint8_t *cell_bits, int blocks_per_patch,
+                     const int32_t *patch_list, int n_list, void *stream);
+
+/* Multi-GPU shadow exchange: copy whole patch blocks of `nplanes` planes
+ * between a pool (plane stride = field_stride) and a packed buffer (plane
+ * stride = packed length); segments = int64 [n][3] (src offset, dst
+ * offset, length).  Patch lists (patch_list/n_list) above restrict a launch
+ * to the patches a rank owns; NULL = every patch of the pool. */
+int mlamr_copy_segments(const double *src, int64_t src_stride, double *dst, int64_t dst_stride,
+                        const int64_t *segments, int n_segments, int max_len, int nplanes,
+                        void *stream);
 
 /* Full reference flag rule on the device (regrid.flag_cells +
  * nesting_allowed, regrid.py:58-101, 185-211): from mlamr_flag_cells' bits,
@@ -202,6 +216,12 @@ int mlamr_cluster_flags(const uint8_t *h_flags, int ny, int nx, double efficienc
  * Returns the count or -1 when it exceeds cap. */
 int mlamr_chop_boxes(const int32_t *h_boxes, int n, int max_nx, int max_ny, int aligned,
                      int32_t *h_out, int cap);
+
+/* Host-side: out[k] = 1 when HOST box a[k] (int64 [na][4], inclusive)
+ * intersects any box of b (multi-GPU shadow planning).  Returns 0, or -1
+ * when the bucket grid would be too large. */
+int mlamr_boxes_meet_any(const int64_t *h_a, int na, const int64_t *h_b, int nb, int bucket,
+                         uint8_t *h_out);
 
 #ifdef __cplusplus
 }

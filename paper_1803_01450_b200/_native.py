@@ -68,26 +68,32 @@ SIGNATURES = {
                                            Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_max_speed_tiles": (ctypes.c_int, [Level, c_vp, c_vp, ctypes.c_int, Params, c_vp, c_vp]),
     "mlamr_fill_ghosts": (ctypes.c_int, [Level, ctypes.POINTER(Level), c_vp, ctypes.c_double,
-                                         ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp]),
+                                         ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp,
+                                         ctypes.c_int, c_vp]),
     "mlamr_fill_bathymetry": (ctypes.c_int, [Level, c_vp, c_i32p, c_vp]),
     "mlamr_average_down": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, Params, c_vp,
                                           ctypes.c_int, c_vp, c_vp]),
     "mlamr_regrid_fill": (ctypes.c_int, [Level, Level, Level, ctypes.c_int, ctypes.c_int, Params,
-                                         c_vp, ctypes.c_int, c_vp, c_vp]),
+                                         c_vp, ctypes.c_int, c_vp, c_vp, ctypes.c_int, c_vp]),
     "mlamr_derefine_delta": (ctypes.c_int, [Level, Level, c_vp, ctypes.c_int, ctypes.c_int, Params,
-                                            c_vp, ctypes.c_int, c_vp]),
+                                            c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp]),
     "mlamr_interpolate_box": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              c_vp, ctypes.c_int, ctypes.c_int, Params,
                                              c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "mlamr_level_reduce": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp]),
-    "mlamr_flag_cells": (ctypes.c_int, [Level, c_vp, Params, c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
+    "mlamr_level_reduce": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp,
+                                          ctypes.c_int, c_vp]),
+    "mlamr_flag_cells": (ctypes.c_int, [Level, c_vp, Params, c_vp, c_vp, c_vp, ctypes.c_int, c_vp,
+                                        ctypes.c_int, c_vp]),
+    "mlamr_copy_segments": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, c_vp, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_flags_reference": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              c_vp, c_vp, c_vp, c_vp]),
     "mlamr_chop_boxes": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         c_vp, ctypes.c_int]),
     "mlamr_step_tile": (ctypes.c_int, [c_vp, c_vp]),
+    "mlamr_boxes_meet_any": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_cluster_flags": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, c_vp,
                                            c_vp, ctypes.c_int]),

@@ -218,3 +218,52 @@ extern "C" int mlamr_chop_boxes(const int32_t *boxes, int n, int max_nx, int max
         for (int q = 0; q < 4; ++q) out[4 * k + q] = res[k][q];
     return (int)res.size();
 }
+
+// For each box of `a` (int64 [na][4], inclusive), does it intersect any box
+// of `b`?  Bucket grid over b's extent (cell `bucket`), CSR of box ids per
+// bucket, exact tests on candidates.  Host-side planning for multi-GPU
+// shadow sets (distributed.py).
+extern "C" int mlamr_boxes_meet_any(const int64_t *a, int na, const int64_t *b, int nb, int bucket,
+                                    uint8_t *out) {
+    for (int k = 0; k < na; ++k) out[k] = 0;
+    if (na == 0 || nb == 0) return 0;
+    int64_t x0 = b[0], y0 = b[1], x1 = b[2], y1 = b[3];
+    for (int k = 1; k < nb; ++k) {
+        x0 = std::min(x0, b[4 * k]);
+        y0 = std::min(y0, b[4 * k + 1]);
+        x1 = std::max(x1, b[4 * k + 2]);
+        y1 = std::max(y1, b[4 * k + 3]);
+    }
+    const int64_t S = bucket > 0 ? bucket : 64;
+    const int64_t gx = (x1 - x0) / S + 1, gy = (y1 - y0) / S + 1;
+    if (gx * gy > (int64_t)1 << 26) return -1;
+    auto bx = [&](int64_t x) { return std::min<int64_t>(gx - 1, std::max<int64_t>(0, (x - x0) / S)); };
+    auto by = [&](int64_t y) { return std::min<int64_t>(gy - 1, std::max<int64_t>(0, (y - y0) / S)); };
+    std::vector<int64_t> cnt(gx * gy + 1, 0);
+    for (int k = 0; k < nb; ++k)
+        for (int64_t j = by(b[4 * k + 1]); j <= by(b[4 * k + 3]); ++j)
+            for (int64_t i = bx(b[4 * k]); i <= bx(b[4 * k + 2]); ++i) cnt[j * gx + i + 1]++;
+    for (int64_t q = 0; q < gx * gy; ++q) cnt[q + 1] += cnt[q];
+    std::vector<int32_t> ids(cnt[gx * gy]);
+    std::vector<int64_t> fill(cnt.begin(), cnt.end() - 1);
+    for (int k = 0; k < nb; ++k)
+        for (int64_t j = by(b[4 * k + 1]); j <= by(b[4 * k + 3]); ++j)
+            for (int64_t i = bx(b[4 * k]); i <= bx(b[4 * k + 2]); ++i) ids[fill[j * gx + i]++] = k;
+#pragma omp parallel for schedule(dynamic, 256)
+    for (int k = 0; k < na; ++k) {
+        const int64_t *A = a + 4 * k;
+        if (A[2] < x0 || A[0] > x1 || A[3] < y0 || A[1] > y1) continue;
+        bool hit = false;
+        for (int64_t j = by(A[1]); j <= by(A[3]) && !hit; ++j)
+            for (int64_t i = bx(A[0]); i <= bx(A[2]) && !hit; ++i)
+                for (int64_t q = cnt[j * gx + i]; q < cnt[j * gx + i + 1]; ++q) {
+                    const int64_t *Bq = b + 4 * ids[q];
+                    if (A[0] <= Bq[2] && Bq[0] <= A[2] && A[1] <= Bq[3] && Bq[1] <= A[3]) {
+                        hit = true;
+                        break;
+                    }
+                }
+        out[k] = hit ? 1 : 0;
+    }
+    return 0;
+}

@@ -132,9 +132,9 @@ template <int M>
 __global__ void __launch_bounds__(NTA) k_fill_ghosts(mlamr_level lv, mlamr_level par, int has_parent,
                                                      const double *par_old, double theta, int r_x,
                                                      int r_y, int4 bcs, mlamr_params prm,
-                                                     const int32_t *status) {
+                                                     const int32_t *status, const int32_t *plist) {
     if (status != nullptr && *status != 0) return;
-    const int p = blockIdx.x;
+    const int p = plist ? plist[blockIdx.x] : (int)blockIdx.x;
     const PatchView pv = patch_view(lv, p);
     const int64_t FS = lv.field_stride;
     const double tol = prm.dry_tolerance;
@@ -258,9 +258,9 @@ __global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_le
 template <int M>
 __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
                                                      int r_x, int r_y, mlamr_params prm,
-                                                     double *refine_delta, int32_t *status) {
+                                                     double *refine_delta, int32_t *status, const int32_t *plist) {
     __shared__ double red[NTA];
-    const int p = blockIdx.y;
+    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
     const PatchView nv = patch_view(nl, p);
     const int cnx = nv.nx / r_x, cny = nv.ny / r_y;
     const int clo_i = floordiv(nv.lo_i, r_x), clo_j = floordiv(nv.lo_j, r_y);
@@ -327,9 +327,9 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
 // but by no new one: coarse mass minus the discarded fine mass.
 template <int M>
 __global__ void __launch_bounds__(NTA) k_derefine(mlamr_level ol, mlamr_level par, const int32_t *new_child,
-                                                  int r_x, int r_y, double *delta) {
+                                                  int r_x, int r_y, double *delta, const int32_t *plist) {
     __shared__ double red[NTA];
-    const int p = blockIdx.y;
+    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
     const PatchView ov = patch_view(ol, p);
     const int cnx = ov.nx / r_x, cny = ov.ny / r_y;
     const int clo_i = floordiv(ov.lo_i, r_x), clo_j = floordiv(ov.lo_j, r_y);
@@ -422,10 +422,10 @@ template <int M>
 __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const double *interior,
                                                       const double *ghosts, const int32_t *child,
                                                       int child_rx, int child_ry, double *patch_mass,
-                                                      int32_t *status) {
+                                                      int32_t *status, const int32_t *plist) {
     __shared__ double red[NTA];
     __shared__ int bad;
-    const int p = blockIdx.y;
+    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
     const PatchView pv = patch_view(lv, p);
     const int64_t FS = lv.field_stride;
     if (threadIdx.x == 0) bad = 0;
@@ -466,8 +466,8 @@ __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const doub
 template <int M>
 __global__ void __launch_bounds__(NTA) k_flag_cells(mlamr_level lv, const double *st, mlamr_params prm,
                                                     const double *eta_rest, const double *wave_tol,
-                                                    uint8_t *bits) {
-    const int p = blockIdx.y;
+                                                    uint8_t *bits, const int32_t *plist) {
+    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
     const PatchView pv = patch_view(lv, p);
     const int64_t FS = lv.field_stride;
     const double tol = prm.dry_tolerance;
@@ -596,15 +596,16 @@ extern "C" int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int
 
 extern "C" int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent, const double *parent_old_state,
                                  double theta, int r_x, int r_y, const int32_t *bcs, mlamr_params prm,
-                                 const int32_t *status, void *stream) {
-    if (lv.num_patches <= 0) return 0;
+                                 const int32_t *status, const int32_t *patch_list, int n_list, void *stream) {
+    const int nb = patch_list ? n_list : lv.num_patches;
+    if (nb <= 0) return 0;
     mlamr_level par = parent ? *parent : lv;
     const int4 b = make_int4(bcs[0], bcs[1], bcs[2], bcs[3]);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_fill_ghosts<M><<<lv.num_patches, NTA, 0, st>>>(lv, par, parent != nullptr, parent_old_state, theta,
-                                                         r_x, r_y, b, prm, status);
+        k_fill_ghosts<M><<<nb, NTA, 0, st>>>(lv, par, parent != nullptr, parent_old_state, theta,
+                                             r_x, r_y, b, prm, status, patch_list);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -634,13 +635,15 @@ extern "C" int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x,
 
 extern "C" int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_level parent, int r_x, int r_y,
                                  mlamr_params prm, double *refine_delta, int blocks_per_patch,
-                                 int32_t *status, void *stream) {
-    if (newlv.num_patches <= 0) return 0;
-    dim3 grid(blocks_per_patch, newlv.num_patches);
+                                 int32_t *status, const int32_t *patch_list, int n_list, void *stream) {
+    const int nb = patch_list ? n_list : newlv.num_patches;
+    if (nb <= 0) return 0;
+    dim3 grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_regrid_fill<M><<<grid, NTA, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status);
+        k_regrid_fill<M><<<grid, NTA, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status,
+                                               patch_list);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -648,13 +651,14 @@ extern "C" int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_lev
 
 extern "C" int mlamr_derefine_delta(mlamr_level oldlv, mlamr_level parent, const int32_t *new_child,
                                     int r_x, int r_y, mlamr_params prm, double *derefine_delta,
-                                    int blocks_per_patch, void *stream) {
-    if (oldlv.num_patches <= 0) return 0;
-    dim3 grid(blocks_per_patch, oldlv.num_patches);
+                                    int blocks_per_patch, const int32_t *patch_list, int n_list, void *stream) {
+    const int nb = patch_list ? n_list : oldlv.num_patches;
+    if (nb <= 0) return 0;
+    dim3 grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta);
+        k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta, patch_list);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -680,14 +684,15 @@ extern "C" int mlamr_interpolate_box(int M, const double *ch, const double *chu,
 
 extern "C" int mlamr_level_reduce(mlamr_level lv, const double *interior_state, const double *ghost_state,
                                   const int32_t *child, double *patch_mass, int blocks_per_patch,
-                                  int32_t *status, void *stream) {
-    if (lv.num_patches <= 0) return 0;
-    dim3 grid(blocks_per_patch, lv.num_patches);
+                                  int32_t *status, const int32_t *patch_list, int n_list, void *stream) {
+    const int nb = patch_list ? n_list : lv.num_patches;
+    if (nb <= 0) return 0;
+    dim3 grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(lv.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
         k_level_reduce<M><<<grid, NTA, 0, st>>>(lv, interior_state, ghost_state, child, 1, 1, patch_mass,
-                                                status);
+                                                status, patch_list);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -695,15 +700,38 @@ extern "C" int mlamr_level_reduce(mlamr_level lv, const double *interior_state, 
 
 extern "C" int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm, const double *eta_rest,
                                 const double *wave_tol, uint8_t *cell_bits, int blocks_per_patch,
-                                void *stream) {
-    if (lv.num_patches <= 0) return 0;
-    dim3 grid(blocks_per_patch, lv.num_patches);
+                                const int32_t *patch_list, int n_list, void *stream) {
+    const int nb = patch_list ? n_list : lv.num_patches;
+    if (nb <= 0) return 0;
+    dim3 grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_flag_cells<M><<<grid, NTA, 0, st>>>(lv, state, prm, eta_rest, wave_tol, cell_bits);
+        k_flag_cells<M><<<grid, NTA, 0, st>>>(lv, state, prm, eta_rest, wave_tol, cell_bits, patch_list);
     });
     if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+// Whole-patch block copies between a pool and a packed exchange buffer (or
+// another pool): seg[3*s] = src offset, seg[3*s+1] = dst offset, seg[3*s+2]
+// = length in elements, applied to every one of `nplanes` planes.
+__global__ void k_copy_segments(const double *__restrict__ src, int64_t src_stride, double *__restrict__ dst,
+                                int64_t dst_stride, const int64_t *__restrict__ seg, int nplanes) {
+    const int sg = blockIdx.y;
+    const int64_t so = seg[3 * sg], doff = seg[3 * sg + 1], len = seg[3 * sg + 2];
+    for (int q = 0; q < nplanes; ++q)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+             i += (int64_t)gridDim.x * blockDim.x)
+            dst[q * dst_stride + doff + i] = src[q * src_stride + so + i];
+}
+
+extern "C" int mlamr_copy_segments(const double *src, int64_t src_stride, double *dst, int64_t dst_stride,
+                                   const int64_t *segments, int n_segments, int max_len, int nplanes,
+                                   void *stream) {
+    if (n_segments <= 0) return 0;
+    dim3 grid((unsigned)std::max(1, std::min(8, (max_len + 255) / 256)), (unsigned)n_segments);
+    k_copy_segments<<<grid, 256, 0, as_stream(stream)>>>(src, src_stride, dst, dst_stride, segments, nplanes);
     return (int)cudaGetLastError();
 }
 

@@ -137,7 +137,11 @@ class LevelPool:
     """All patches of one level, resident on the device."""
 
     def __init__(self, spec: LevelSpec, boxes, M: int, device: torch.device,
-                 stream: torch.cuda.Stream, need_gown: bool):
+                 stream: torch.cuda.Stream, need_gown: bool, owned: Optional[np.ndarray] = None,
+                 gidx: Optional[np.ndarray] = None):
+        """``owned`` (bool per patch) restricts stepping, filling, flagging and
+        reductions to this rank's patches in a sharded run (the others are
+        shadows, distributed.py); ``gidx`` = global indices of the patches."""
         self.spec = spec
         self.M = M
         self.device = device
@@ -145,9 +149,12 @@ class LevelPool:
         b = np.asarray(boxes, dtype=np.int64).reshape(-1, 4)
         self.boxes = b
         self.P = len(b)
+        self.gidx = np.arange(self.P, dtype=np.int64) if gidx is None else np.asarray(gidx, np.int64)
+        self.owned = None if owned is None else np.asarray(owned, bool)
         nx = b[:, 2] - b[:, 0] + 1
         ny = b[:, 3] - b[:, 1] + 1
-        self.ncells = int((nx * ny).sum())
+        cells = nx * ny
+        self.ncells = int(cells.sum() if self.owned is None else cells[self.owned].sum())
         size = (nx + 2 * GHOST_WIDTH) * (ny + 2 * GHOST_WIDTH)
         aligned = (size + ALIGN - 1) // ALIGN * ALIGN
         self.offsets = np.concatenate([[0], np.cumsum(aligned)[:-1]]).astype(np.int64) if self.P else \
@@ -165,10 +172,19 @@ class LevelPool:
             self.box_d = A.upload(b.astype(np.int32), device, stream)
             self.off_d = A.upload(self.offsets, device, stream)
             tl = tile_list(b)
+            if self.owned is not None and len(tl):
+                tl = tl[self.owned[tl[:, 0]]]
             self.tiles = tl
             self.n_tiles = len(tl)
             self.tiles_d = A.upload(tl, device, stream) if len(tl) else torch.zeros(3, dtype=torch.int32, device=device)
             self.tile_acc = torch.zeros(max(self.n_tiles, 1) * (M + 2), dtype=torch.float64, device=device)
+            self.owned_d = None
+            self.n_owned = self.P
+            if self.owned is not None:
+                ol = np.flatnonzero(self.owned).astype(np.int32)
+                self.n_owned = len(ol)
+                self.owned_d = A.upload(ol, device, stream) if len(ol) else \
+                    torch.zeros(1, dtype=torch.int32, device=device)
             self.speed_bits = torch.full((max(self.P, 1),), -1, dtype=torch.int64, device=device)
             mapn = (spec.nx + 2 * GHOST_WIDTH) * (spec.ny + 2 * GHOST_WIDTH)
             self.own = acquire(mapn, torch.int32, device, stream).fill_(-1)
@@ -220,6 +236,29 @@ class LevelPool:
         lv.own = self.own.data_ptr()
         lv.gown = self.gown.data_ptr() if self.gown is not None else None
         return lv
+
+    def work_list(self):
+        """(device patch-list pointer, count) of the patches this rank owns,
+        or (None, 0) when it owns them all (single-GPU runs)."""
+        if self.owned_d is None:
+            return None, 0
+        return self.owned_d.data_ptr(), self.n_owned
+
+    def local_of(self, g: np.ndarray) -> np.ndarray:
+        """Local indices of global patch indices (all must be held)."""
+        return np.searchsorted(self.gidx, g)
+
+    def copy_segments(self, src_buf, src_stride, dst_buf, dst_stride, src_off, dst_off, sizes) -> None:
+        """Whole-block copies of all 3M planes (multi-GPU shadow exchange)."""
+        n = len(sizes)
+        if n == 0:
+            return
+        seg = np.stack([np.asarray(src_off, np.int64), np.asarray(dst_off, np.int64),
+                        np.asarray(sizes, np.int64)], axis=1)
+        seg_d = arena().upload(seg, self.device, self.stream)
+        N.check(N.lib().mlamr_copy_segments(src_buf.data_ptr(), int(src_stride), dst_buf.data_ptr(),
+                                            int(dst_stride), seg_d.data_ptr(), n, int(np.max(sizes)),
+                                            3 * self.M, self.stream.cuda_stream), "copy_segments")
 
     def blocks_per_patch(self, cells: int) -> int:
         return int(max(1, min(64, (cells + NTHREADS - 1) // NTHREADS)))

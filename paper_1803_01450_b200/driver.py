@@ -171,11 +171,12 @@ class Simulation:
             return torch.zeros(self.M, dtype=torch.float64, device=self.dev)
         bpp = pool.blocks_per_patch(pool.max_cells)
         with torch.cuda.stream(self.stream):
-            part = torch.empty(pool.P * bpp * self.M, dtype=torch.float64, device=self.dev)
+            part = torch.zeros(pool.P * bpp * self.M, dtype=torch.float64, device=self.dev)
             ghosts = pool.state if pool.ghosts_in_cur else pool.other
             child = pool.child.data_ptr() if pool.child is not None else None
+            pl, nl = pool.work_list()
             self._call(self.lib.mlamr_level_reduce, pool.struct(), pool.state.data_ptr(), ghosts.data_ptr(),
-                       child, part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
+                       child, part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
             s = self.spec(level)
             return part.view(-1, self.M).sum(dim=0) * (s.dx * s.dy)
 
@@ -209,8 +210,9 @@ class Simulation:
                 t0, dt, old = st
                 theta = min(1.0, max(0.0, (t - t0) / dt)) if dt > 0 else 1.0
                 old_ptr = old.data_ptr()
+        pl, nl = pool.work_list()
         self._call(self.lib.mlamr_fill_ghosts, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
-                   self.prm, self.status.data_ptr(), self.sh)
+                   self.prm, self.status.data_ptr(), pl, nl, self.sh)
         pool.ghosts_in_cur = True
 
     # -- regridding (driver.py:192-222, regrid.py:235-353) -------------------------
@@ -259,9 +261,10 @@ class Simulation:
             b = self._flag_buffers(level)
             with torch.cuda.stream(self.stream):
                 b["bits"].zero_()
+                pl, nl = pool.work_list()
                 self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
                            self._eta_rest.data_ptr(), self._wave_tol.data_ptr(), b["bits"].data_ptr(),
-                           pool.blocks_per_patch(pool.max_interior), self.sh)
+                           pool.blocks_per_patch(pool.max_interior), pl, nl, self.sh)
                 self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
                            self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
                            b["scratch"].data_ptr(), self.sh)
@@ -330,16 +333,18 @@ class Simulation:
                 part = torch.zeros(new.P * bpp * M, dtype=torch.float64, device=self.dev)
                 fs = self.spec(level + 1)
                 ol = old.struct() if old is not None else empty_level_struct(fs, M)
+                pl, nl = new.work_list()
                 self._call(self.lib.mlamr_regrid_fill, new.struct(), ol, par.struct(), rx, ry, self.prm,
-                           part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
+                           part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
                 if not init:
                     self.delta_acc[0] += part.view(-1, M).sum(dim=0)
             new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
             if old is not None and old.P and not init:
                 bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
                 part = torch.zeros(old.P * bpp * M, dtype=torch.float64, device=self.dev)
+                pl, nl = old.work_list()
                 self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
-                           rx, ry, self.prm, part.data_ptr(), bpp, self.sh)
+                           rx, ry, self.prm, part.data_ptr(), bpp, pl, nl, self.sh)
                 self.delta_acc[1] += part.view(-1, M).sum(dim=0)
         self.host_prof["regrid.fill+derefine"] += time.perf_counter() - tq
         tq = time.perf_counter()

@@ -334,7 +334,7 @@ def fill_ghosts(patch, siblings, parent_provider, boundaries, level_box, r_x: in
     lv = pool.struct()
     lv.num_patches = 1  # fill only `patch`; the others serve as siblings
     N.check(N.lib().mlamr_fill_ghosts(lv, None, None, 0.0, 1, 1, N.bc_array(boundaries), _params(params),
-                                      None, torch.cuda.current_stream().cuda_stream), "fill_ghosts")
+                                      None, None, 0, torch.cuda.current_stream().cuda_stream), "fill_ghosts")
     host = pool.download()
     h, hu, hv, _ = pool.patch_arrays(0, host=host)
     patch.h[...] = h

@@ -1,0 +1,348 @@
+"""Multi-GPU driver: the subcycled recursion of :class:`driver.Simulation`
+over SFC-sharded patch ownership with shadow replicas (distributed.py).
+
+Differences from the single-GPU driver, all confined to this subclass:
+
+* every level keeps its global layout and owner array; the local pool
+  holds owned + shadow patches in global list order, so the owner maps'
+  precedence equals the reference's list order (ghost.py:58-84);
+* stepping, filling, flagging and reductions run over owned patches only
+  (patch lists / owned tiles); coarsening runs over every local fine
+  patch into the local coarse pool, and the coarse owner's result counts;
+* shadows are refreshed by whole-patch transfers from their owners
+  (i) at the start of a level's advance, (ii) after its t0 ghost fill
+  (their frames then sit in the buffer that becomes the stash),
+  (iii) after its t1 fill, and (iv) for the finer level before it is
+  averaged down;
+* a regrid all-reduces the flag bits, clusters identically on every rank,
+  partitions the new layout along the Morton curve and reshapes the
+  affected pools (parents of old and new owned patches, old patches
+  overlapping new owned ones, children needed by new coarse owners);
+* dt / dynamic-r_t speeds are all-reduced maxima, composite mass and
+  counters all-reduced sums, the status word an all-reduced maximum.
+"""
+
+from __future__ import annotations
+
+from math import prod
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _native as N
+from .device import LevelPool, empty_level_struct, paint_child_map
+from .distributed import (Comm, _any_meet, needed, partition, patch_sizes, plan_acquire, plan_refresh,
+                          run_transfer)
+from .driver import Simulation
+from .mesh import GHOST_WIDTH, IndexBox, boxes_array
+from .regrid import chop_boxes, cluster_boxes
+
+_EMPTY = np.zeros((0, 4), np.int64)
+
+
+class ShardedSimulation(Simulation):
+    def __init__(self, problem, comm: Comm | None = None, device: str = "cuda", stream=None):
+        self.comm = comm or Comm()
+        self.rank, self.world = self.comm.rank, self.comm.world
+        self.layout, self.owner, self.held = {}, {}, {}
+        self.bytes_exchanged = 0
+        self._common_init(problem, device, stream)
+        if self.pb.flag_rule[0] == "gradient":
+            raise NotImplementedError("sharded runs support the reference and Bernoulli flag rules")
+        b1 = boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)])
+        self.layout[1] = b1
+        self.owner[1] = np.zeros(1, np.int32)
+        self.held[1] = {r: (np.arange(1) if r == 0 else np.zeros(0, np.int64)) for r in range(self.world)}
+        base = self._make_pool(1, b1, self.owner[1], self.held[1][self.rank])
+        self._set_initial(base)
+        self.levels[1] = base
+        for lev in range(1, self.L):
+            self._rebuild(lev, init=True)
+        self._mass_prev = self.composite_mass()
+        self.stats.initial_mass = list(self._mass_prev)
+
+    # -- geometry helpers -----------------------------------------------------
+    def _scale(self, level: int):
+        sx = prod(s.r_x for s in self.specs[level - 1:self.L - 1])
+        sy = prod(s.r_y for s in self.specs[level - 1:self.L - 1])
+        return sx, sy
+
+    def _ratios(self):
+        return {s.level: (s.r_x, s.r_y) for s in self.specs}
+
+    def _held_all(self, level, layouts, owners, extra=None):
+        R = self._ratios()
+        return {r: needed(level, r, layouts, owners, R, None if extra is None else extra(r))
+                for r in range(self.world)}
+
+    def _make_pool(self, level, gboxes, owner, local_g) -> LevelPool:
+        local_g = np.asarray(local_g, np.int64)
+        pool = LevelPool(self.spec(level), gboxes[local_g] if len(local_g) else _EMPTY, self.M, self.dev,
+                         self.stream, need_gown=level < self.L, owned=owner[local_g] == self.rank,
+                         gidx=local_g)
+        if pool.P:
+            self._call(self.lib.mlamr_fill_bathymetry, pool.struct(), self.level_bathy[level - 1].data_ptr(),
+                       self.bcs, self.sh)
+        return pool
+
+    # -- shadow transfers --------------------------------------------------------
+    def _transfer(self, level, tr, src: LevelPool, dst: LevelPool) -> None:
+        sizes = patch_sizes(self.layout[level])
+        M3 = 3 * self.M
+
+        def pack(g, src_off, buf):
+            sz = sizes[g]
+            n = int(sz.sum())
+            poff = np.concatenate([[0], np.cumsum(sz)[:-1]])
+            src.copy_segments(src.state, src.FS, buf, n, src_off, poff, sz)
+
+        def unpack(g, buf, dst_off):
+            sz = sizes[g]
+            n = int(sz.sum())
+            poff = np.concatenate([[0], np.cumsum(sz)[:-1]])
+            dst.copy_segments(buf, n, dst.state, dst.FS, poff, dst_off, sz)
+
+        with torch.cuda.stream(self.stream):
+            self.bytes_exchanged += run_transfer(
+                self.comm, tr, sizes, M3, lambda g: src.offsets[src.local_of(g)],
+                lambda g: dst.offsets[dst.local_of(g)], pack, unpack, torch.float64, self.dev)
+
+    def _refresh(self, level: int) -> None:
+        if self.world == 1 or level not in self.levels:
+            return
+        tr = plan_refresh(self.rank, self.world, self.held[level], self.owner[level])
+        pool = self.levels[level]
+        self._transfer(level, tr, pool, pool)
+
+    def _reshape(self, level: int, new_held) -> None:
+        """Replace a level's local pool by one holding new_held[rank] (same
+        layout and owners), moving data: local copies + owners' sends."""
+        old = self.levels[level]
+        want = new_held[self.rank]
+        # the skip must be a collective decision: a rank whose own set is
+        # unchanged may still have to send patches to a rank whose set grew
+        if all(np.array_equal(new_held[r], self.held[level][r]) for r in range(self.world)):
+            self.held[level] = new_held
+            return
+        new = self._make_pool(level, self.layout[level], self.owner[level], want)
+        common = np.intersect1d(old.gidx, want, assume_unique=True)
+        if len(common):
+            sizes = patch_sizes(self.layout[level])[common]
+            with torch.cuda.stream(self.stream):
+                new.copy_segments(old.state, old.FS, new.state, new.FS, old.offsets[old.local_of(common)],
+                                  new.offsets[new.local_of(common)], sizes)
+        tr = plan_acquire(self.rank, self.world, self.held[level], new_held, self.owner[level])
+        self._transfer(level, tr, old, new)
+        new.time = old.time
+        new.ghosts_in_cur = old.ghosts_in_cur
+        new.child = old.child
+        self.levels[level] = new
+        self.held[level] = new_held
+        old.release()
+
+    # -- reductions ------------------------------------------------------------------
+    def _sync_status(self, where: str = "") -> None:
+        with torch.cuda.stream(self.stream):
+            self.comm.allreduce(self.status, dist.ReduceOp.MAX if self.world > 1 else None)
+            self.comm.allreduce(self.bad, dist.ReduceOp.MIN if self.world > 1 else None)
+        super()._sync_status(where)
+
+    def composite_mass(self) -> np.ndarray:
+        with torch.cuda.stream(self.stream):
+            tot = torch.zeros(self.M, dtype=torch.float64, device=self.dev)
+            for lev in range(1, self.L + 1):
+                if lev in self.levels:
+                    tot = tot + self._level_reduce(lev)
+            self.comm.allreduce(tot)
+        self.stream.synchronize()
+        from .device import arena
+        arena().reset()
+        return tot.cpu().numpy()
+
+    def level_speed(self, level: int):
+        pool = self.levels.get(level)
+        with torch.cuda.stream(self.stream):
+            best = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
+            if pool is not None and pool.P:
+                pool.speed_bits.fill_(-1)
+                if pool.n_tiles:
+                    self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(),
+                               pool.tiles_d.data_ptr(), pool.n_tiles, self.prm, pool.speed_bits.data_ptr(),
+                               self.sh)
+                best = torch.max(pool.speed_bits[:pool.P]).reshape(1)
+            self.comm.allreduce(best, dist.ReduceOp.MAX if self.world > 1 else None)
+        self.stream.synchronize()
+        b = int(best.item())
+        # stable_dt is monotone in the speed, so the minimum over patches of
+        # the per-patch dt equals dt of the global maximum speed (bit for bit)
+        return np.array([0.0 if b < 0 else np.array([b], np.int64).view(np.float64)[0]])
+
+    def finish(self):
+        with torch.cuda.stream(self.stream):
+            self.comm.allreduce(self.acc)
+            self.comm.allreduce(self.delta_acc)
+            cells = torch.tensor([float(self.stats.total_cell_updates)], dtype=torch.float64, device=self.dev)
+            self.comm.allreduce(cells)
+        st = super().finish()
+        st.total_cell_updates = int(cells.item())
+        return st
+
+    # -- flags over owned patches, all-reduced -----------------------------------------
+    def flags_and_allowed(self, level: int):
+        s = self.spec(level)
+        if self.pb.flag_rule[0] != "reference":
+            from .mesh import dilate, paint
+            from .regrid import nesting_allowed
+            covered = paint(self.layout[level], s.ny, s.nx)
+            f = self.pb.bernoulli_flags(level, self.steps[level])
+            f = dilate(f, self.pb.flag_rule[2]) & covered
+            allowed = nesting_allowed(self.layout[level], s.ny, s.nx)
+            return f & allowed, allowed
+        pool = self.levels[level]
+        b = self._flag_buffers(level)
+        with torch.cuda.stream(self.stream):
+            b["bits"].zero_()
+            pl, nl = pool.work_list()
+            if pool.P and (pl is None or nl > 0):
+                self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
+                           self._eta_rest.data_ptr(), self._wave_tol.data_ptr(), b["bits"].data_ptr(),
+                           pool.blocks_per_patch(pool.max_interior), pl, nl, self.sh)
+            if self.world > 1:
+                wide = b["bits"].to(torch.int32)
+                self.comm.allreduce(wide, dist.ReduceOp.MAX)
+                b["bits"].copy_(wide.to(torch.uint8))
+            self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
+                       self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
+                       b["scratch"].data_ptr(), self.sh)
+            b["flags_h"].copy_(b["flags"], non_blocking=True)
+            b["allowed_h"].copy_(b["allowed"], non_blocking=True)
+        self.stream.synchronize()
+        return (b["flags_h"].numpy().reshape(s.ny, s.nx).view(np.bool_),
+                b["allowed_h"].numpy().reshape(s.ny, s.nx).view(np.bool_))
+
+    # -- regrid --------------------------------------------------------------------------
+    def _rebuild(self, level: int, init: bool = False) -> bool:
+        s = self.spec(level)
+        rx, ry = s.r_x, s.r_y
+        fixed = self.pb.fixed_layout(level + 1) if init else None
+        if fixed is not None:
+            fb = np.asarray(fixed, dtype=np.int64).reshape(-1, 4)
+            cb = np.stack([fb[:, 0] // rx, fb[:, 1] // ry, (fb[:, 2] + 1) // rx - 1, (fb[:, 3] + 1) // ry - 1], 1)
+            cb = self._lexsorted(cb)
+        else:
+            flags, allowed = self.flags_and_allowed(level)
+            cb = cluster_boxes(flags, self.pb.efficiency_target, allowed)
+            if self.pb.max_patch is not None:
+                cb = chop_boxes(cb, *self.pb.max_patch, aligned=self.pb.chop_aligned)
+        cb = np.asarray(cb, dtype=np.int64).reshape(-1, 4)
+        nboxes = np.stack([cb[:, 0] * rx, cb[:, 1] * ry, (cb[:, 2] + 1) * rx - 1, (cb[:, 3] + 1) * ry - 1], 1)
+        old_layout = self.layout.get(level + 1, _EMPTY)
+        old_owner = self.owner.get(level + 1, np.zeros(0, np.int32))
+        if level + 1 in self.levels:
+            if len(old_layout) == len(nboxes) and np.array_equal(self._lexsorted(old_layout),
+                                                                 self._lexsorted(nboxes)):
+                return False
+        elif len(nboxes) == 0:
+            return False
+        new_owner = partition(nboxes, *self._scale(level + 1), self.world)
+        layouts = dict(self.layout)
+        owners = dict(self.owner)
+        layouts[level + 1] = nboxes
+        owners[level + 1] = new_owner
+        # (a) the parent level must hold the stencils of new and old owned fine patches
+        self._reshape(level, self._held_all(level, layouts, owners,
+                                            lambda r: {level + 1: old_layout[old_owner == r]}))
+        par = self.levels[level]
+        # (b) old fine patches overlapping new owned patches
+        old = self.levels.get(level + 1)
+        if old is not None:
+            ext = {}
+            for r in range(self.world):
+                hit = np.flatnonzero(_any_meet(old_layout, nboxes[new_owner == r]))
+                ext[r] = np.union1d(self.held[level + 1][r], hit).astype(np.int64)
+            self._reshape(level + 1, ext)
+            old = self.levels[level + 1]
+        # (c) the new level
+        held_new = self._held_all(level + 1, layouts, owners)
+        new = self._make_pool(level + 1, nboxes, new_owner, held_new[self.rank])
+        new.time = par.time
+        M = self.M
+        with torch.cuda.stream(self.stream):
+            if init and fixed is None and self.pb.init_mode == "scenario":
+                self._set_initial(new)
+            elif new.P:
+                bpp = new.blocks_per_patch(new.max_interior // (rx * ry))
+                part = torch.zeros(new.P * bpp * M, dtype=torch.float64, device=self.dev)
+                ol = old.struct() if old is not None else empty_level_struct(self.spec(level + 1), M)
+                pl, nl = new.work_list()
+                if nl > 0:
+                    self._call(self.lib.mlamr_regrid_fill, new.struct(), ol, par.struct(), rx, ry, self.prm,
+                               part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
+                if not init:
+                    self.delta_acc[0] += part.view(-1, M).sum(dim=0)
+            new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
+            if old is not None and old.P and not init:
+                bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
+                part = torch.zeros(old.P * bpp * M, dtype=torch.float64, device=self.dev)
+                pl, nl = old.work_list()
+                if nl > 0:
+                    self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
+                               rx, ry, self.prm, part.data_ptr(), bpp, pl, nl, self.sh)
+                self.delta_acc[1] += part.view(-1, M).sum(dim=0)
+        # (d) install and fill the new shadows from their owners
+        self.layout[level + 1] = nboxes
+        self.owner[level + 1] = new_owner
+        self.held[level + 1] = held_new
+        self.levels[level + 1] = new
+        if old is not None:
+            old.release()
+        par.child = new_child
+        self._refresh(level + 1)
+        # (e) the level below the new one: its shadow set depends on the new owners
+        if level + 2 in self.levels:
+            self._reshape(level + 2, self._held_all(level + 2, layouts, owners))
+            fs = self.spec(level + 1)
+            new.child = paint_child_map(fs, self.layout[level + 2], fs.r_x, fs.r_y, self.dev, self.stream)
+        if not init:
+            self.stats.num_regrids += 1
+        return True
+
+    # -- recursion with refresh points -------------------------------------------------
+    def advance_level(self, level: int, dt: float, t0: float) -> None:
+        self._refresh(level)                                            # (i)
+        if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:
+            self.regrid_from(level)
+        self.fill_level_ghosts(level, t0)
+        self._refresh(level)                                            # (ii)
+        pool = self.levels[level]
+        child = self.levels.get(level + 1)
+        has_child = child is not None and len(self.layout.get(level + 1, _EMPTY)) > 0
+        self._step_patches(level, dt)
+        self.steps[level] += 1
+        t1 = t0 + dt
+        pool.time = t1
+        if has_child:
+            self.fill_level_ghosts(level, t1)
+            self._refresh(level)                                        # (iii)
+            self._stash[level] = (t0, dt, pool.other)
+            s = self.spec(level)
+            dtf = dt / s.r_t
+            for k in range(s.r_t):
+                self.advance_level(level + 1, dtf, t0 + k * dtf)
+            self.levels[level + 1].time = t1
+            self._refresh(level + 1)                                    # (iv)
+            self._average_down(level)
+            del self._stash[level]
+
+    def owned_fields(self, level: int):
+        """{global index: (box, h, hu, hv, bathy)} of this rank's patches."""
+        pool = self.levels[level]
+        host = pool.download()
+        out = {}
+        for p in range(pool.P):
+            if pool.owned is not None and not pool.owned[p]:
+                continue
+            h, hu, hv, b = pool.patch_arrays(p, host=host)
+            out[int(pool.gidx[p])] = (tuple(int(v) for v in pool.boxes[p]), h, hu, hv, b)
+        return out

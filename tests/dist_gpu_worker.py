@@ -1,0 +1,85 @@
+"""Worker for tests/test_gpu_sharded.py (run under torchrun, gloo backend).
+
+Each rank runs the sharded driver over its share of the patches and, in the
+same process, the single-GPU driver over all of them; after every coarse
+step every owned patch must be bit-identical, and the all-reduced
+statistics must equal the single-GPU ones."""
+
+import os
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(HERE))
+sys.path.insert(0, HERE)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def variant(name):
+    from paper_1803_01450_b200 import problems
+    if name == "C2":
+        pb = problems.config2()
+        pb.regrid_interval = 2
+        return pb, 3
+    if name == "C4":
+        pb = problems.config4(nx0=64)
+        pb.regrid_interval = 2
+        return pb, 2
+    if name == "C5":
+        pb = problems.config5(nx0=64)
+        pb.bernoulli = (0.05,)
+        return pb, 3
+    raise KeyError(name)
+
+
+def main():
+    name = sys.argv[1]
+    from datetime import timedelta
+    dist.init_process_group("gloo", timeout=timedelta(seconds=120))
+    torch.cuda.set_device(0)
+    from paper_1803_01450_b200.driver import Simulation
+    from paper_1803_01450_b200.sharded import ShardedSimulation
+    pb, steps = variant(name)
+    ref = Simulation(pb, stream=torch.cuda.Stream())
+    sh = ShardedSimulation(pb, stream=torch.cuda.Stream())
+    rank = dist.get_rank()
+
+    def compare(tag):
+        bad = 0
+        for lev in range(1, ref.L + 1):
+            if lev not in ref.levels:
+                continue
+            full = ref.patch_fields(lev)
+            gl = sh.layout.get(lev, np.zeros((0, 4)))
+            assert [tuple(int(v) for v in b) for b in gl] == [f[0] for f in full], (tag, lev, "layout")
+            for g, (box, h, hu, hv, b) in sh.owned_fields(lev).items():
+                R = full[g]
+                for a, c in ((h, R[1]), (hu, R[2]), (hv, R[3])):
+                    x, y = a[:, 2:-2, 2:-2], c[:, 2:-2, 2:-2]
+                    if not np.array_equal(x, y):
+                        bad += 1
+        assert bad == 0, (tag, rank, bad)
+
+    compare("init")
+    for k in range(steps):
+        dt = ref.choose_dt()
+        assert sh.choose_dt() == dt, k
+        ref.apply_dynamic_rt(dt)
+        sh.apply_dynamic_rt(dt)
+        ref.advance_coarse_step(dt)
+        sh.advance_coarse_step(dt)
+        compare(f"step{k}")
+    a, b = ref.finish(), sh.finish()
+    assert a.total_cell_updates == b.total_cell_updates, (a.total_cell_updates, b.total_cell_updates)
+    assert a.num_regrids == b.num_regrids
+    np.testing.assert_allclose(sh.composite_mass(), ref.composite_mass(), rtol=1e-12)
+    print(f"rank {rank}: {name} sharded == single-GPU ({steps} steps, exchanged {sh.bytes_exchanged} B, "
+          f"owned {[int(p.n_owned) for p in sh.levels.values()]} of {[len(v) for v in sh.layout.values()]})",
+          flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

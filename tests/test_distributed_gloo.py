@@ -1,0 +1,154 @@
+"""Multi-rank host logic of the sharded path (distributed.py) with the gloo
+backend on CPU, world size 2: SFC partition, shadow rules, transfer plans
+and the whole-patch exchange (with host tensors standing in for device
+pools; the CUDA pack kernel is exercised by tests/test_gpu_sharded.py)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _layouts():
+    """A 3-level layout on a 64^2 level-1 grid, r=4: level-2/3 boxes chopped
+    from a few blobs (deterministic)."""
+    rng = np.random.default_rng(5)
+    L2 = []
+    for j in range(8, 56, 8):
+        for i in range(4, 60, 8):
+            if rng.random() < 0.6:
+                L2.append((4 * i, 4 * j, 4 * i + 31, 4 * j + 31))
+    L2 = np.array(sorted(L2, key=lambda b: (b[1], b[0])), np.int64)
+    L3 = []
+    for b in L2[::2]:
+        for dj in (0, 64):
+            for di in (0, 64):
+                L3.append((4 * b[0] + 16 + di, 4 * b[1] + 16 + dj, 4 * b[0] + 16 + di + 47, 4 * b[1] + 16 + dj + 47))
+    L3 = np.array(sorted(L3, key=lambda b: (b[1], b[0])), np.int64)
+    return {1: np.array([[0, 0, 63, 63]], np.int64), 2: L2, 3: L3}
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1803_01450_b200.distributed import (Comm, needed, partition, patch_sizes, plan_acquire,
+                                                       plan_refresh, run_transfer)
+        comm = Comm()
+        assert comm.world == world and comm.rank == rank
+        layouts = _layouts()
+        ratios = {1: (4, 4), 2: (4, 4), 3: (1, 1)}
+        owners = {1: np.zeros(1, np.int32), 2: partition(layouts[2], 4, 4, world),
+                  3: partition(layouts[3], 1, 1, world)}
+        held = {lv: {r: needed(lv, r, layouts, owners, ratios) for r in range(world)} for lv in (1, 2, 3)}
+        M3 = 6
+        results = {}
+        for lv in (2, 3):
+            B = layouts[lv]
+            sizes = patch_sizes(B)
+            mine = held[lv][rank]
+            offs = np.concatenate([[0], np.cumsum(sizes[mine])[:-1]]).astype(np.int64)
+            FS = int(sizes[mine].sum()) + 1
+            pool = torch.full((M3, FS), -1.0, dtype=torch.float64)
+            for k, g in enumerate(mine):
+                if owners[lv][g] == rank:   # owners know their data: a function of (g, plane, cell)
+                    vals = g * 1000.0 + torch.arange(M3 * int(sizes[g]), dtype=torch.float64).reshape(M3, -1)
+                    pool[:, offs[k]:offs[k] + sizes[g]] = vals
+            loc = {int(g): int(o) for g, o in zip(mine, offs)}
+            flat = pool.view(-1)
+
+            def pack(g, src_off, buf):
+                n = int(sizes[g].sum())
+                b2 = buf.view(M3, n)
+                at = 0
+                for gg, so in zip(g, src_off):
+                    b2[:, at:at + sizes[gg]] = pool[:, so:so + sizes[gg]]
+                    at += int(sizes[gg])
+
+            def unpack(g, buf, dst_off):
+                n = int(sizes[g].sum())
+                b2 = buf.view(M3, n)
+                at = 0
+                for gg, do in zip(g, dst_off):
+                    pool[:, do:do + sizes[gg]] = b2[:, at:at + sizes[gg]]
+                    at += int(sizes[gg])
+
+            offs_of = lambda g: np.array([loc[int(x)] for x in g], np.int64)
+            tr = plan_refresh(rank, world, held[lv], owners[lv])
+            run_transfer(comm, tr, sizes, M3, offs_of, offs_of, pack, unpack, torch.float64, "cpu")
+            ok = True
+            for k, g in enumerate(mine):
+                vals = g * 1000.0 + torch.arange(M3 * int(sizes[g]), dtype=torch.float64).reshape(M3, -1)
+                ok &= bool(torch.equal(pool[:, offs[k]:offs[k] + sizes[g]], vals))
+            results[lv] = (ok, len(mine), int((owners[lv][mine] == rank).sum()))
+        # acquire plan symmetry: what rank r receives from s equals what s sends to r
+        want = {r: np.union1d(held[3][r], np.arange(min(3, len(layouts[3])))) for r in range(world)}
+        tr = plan_acquire(rank, world, held[3], want, owners[3])
+        sent = {q: g.tolist() for q, g in tr.send.items()}
+        recv = {q: g.tolist() for q, g in tr.recv.items()}
+        t = torch.tensor([comm.allreduce(torch.ones(1)).item()])
+        q.put((rank, results, sent, recv, t.item()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_exchange_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(world):
+        r, res, sent, recv, t = q.get(timeout=120)
+        out[r] = (res, sent, recv, t)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    shadows = {2: 0, 3: 0}
+    for r in range(world):
+        res, sent, recv, t = out[r]
+        assert t == world
+        for lv, (ok, held_n, owned_n) in res.items():
+            assert ok, (r, lv)
+            assert owned_n > 0, (r, lv)
+            shadows[lv] += held_n - owned_n
+    assert all(v > 0 for v in shadows.values()), shadows   # the exchange had work to do
+    # plans are mutually consistent
+    for r in range(world):
+        for s_ in range(world):
+            if r == s_:
+                continue
+            assert out[r][1].get(s_, []) == out[s_][2].get(r, [])
+
+
+def test_partition_balance_and_locality():
+    from paper_1803_01450_b200.distributed import morton, partition
+    assert morton(np.array([1]), np.array([0]))[0] == 1 and morton(np.array([0]), np.array([1]))[0] == 2
+    g = np.arange(0, 1024, 32)
+    I, J = np.meshgrid(g, g)
+    B = np.stack([I.ravel(), J.ravel(), I.ravel() + 31, J.ravel() + 31], 1)
+    for world in (2, 4, 8):
+        own = partition(B, 1, 1, world)
+        cnt = np.bincount(own, minlength=world)
+        assert cnt.max() - cnt.min() <= 1
+        # Z-order spans of a square grid are compact: each rank's bounding box is
+        # at most twice its share of the area
+        for r in range(world):
+            b = B[own == r]
+            area = (b[:, 2].max() - b[:, 0].min() + 1) * (b[:, 3].max() - b[:, 1].min() + 1)
+            assert area <= 2.0 * 1024 * 1024 / world
