@@ -11,9 +11,8 @@ the subcycled ghost fills / patch steps of all levels and the coarsenings
 (driver.py:299-309 of the reference).  The reference arm (``--impl
 reference``) times the oracle port of the reference's CPU algorithm
 (oracle/, C + numpy, all host threads) on a bounded sample of the same
-workload.  Multi-GPU (torchrun, N>1): each rank advances its own replica
-of the workload (weak scaling, no data-path collective yet) and the
-timed region is the max over ranks.
+workload.  Multi-GPU (torchrun, N>1): one C4 problem whose patches are sharded along a Morton curve (sharded.py),
+shadow halos move over NCCL, and the timed region is the max over ranks.
 """
 
 from __future__ import annotations
@@ -102,8 +101,8 @@ def coarse_step(sim):
 
 def step_bytes(pool, M):
     """Algorithmic HBM bytes of one step launch on a level:
-    8*[(3M+1)*(nx+2)(ny+2) + 3M*nx*ny] per patch."""
-    b = pool.boxes
+    8*[(3M+1)*(nx+2)(ny+2) + 3M*nx*ny] per stepped (owned) patch."""
+    b = pool.boxes if pool.owned is None else pool.boxes[pool.owned]
     nx = b[:, 2] - b[:, 0] + 1
     ny = b[:, 3] - b[:, 1] + 1
     return int((8 * ((3 * M + 1) * (nx + 2) * (ny + 2) + 3 * M * nx * ny)).sum())
@@ -177,14 +176,25 @@ def b200_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("MLAMR_DIST_BACKEND", "nccl")   # gloo: test ranks sharing one GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     pb = problems.CONFIGS[args.config]()
     M = pb.num_layers
     stream = torch.cuda.Stream()
-    sim = Simulation(pb, stream=stream)
+    if world > 1:
+        # SFC-sharded patches over NCCL (strong scaling: one C4 problem)
+        from paper_1803_01450_b200.sharded import ShardedSimulation
+        dist.barrier()
+        sim = ShardedSimulation(pb, stream=stream)
+    else:
+        sim = Simulation(pb, stream=stream)
     L = sim.L
     for _ in range(args.warmup):
         coarse_step(sim)
@@ -244,7 +254,10 @@ def b200_arm(args):
 
     # ---- e2e: host buffers -> device -> K steps -> host ---------------------
     e2e = None
-    if not args.no_e2e:
+    if world > 1:
+        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
+               "unavailable": "sharded snapshot/restore not implemented yet"}
+    if not args.no_e2e and world == 1:
         snap = sim.snapshot()
         torch.cuda.synchronize()
         if world > 1:
@@ -281,12 +294,15 @@ def b200_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": f"{args.config}: {pb.num_levels} levels, M={M}, "
                                    f"L1 {pb.coarse_nx}x{pb.coarse_ny}, ratios {pb.ratios_x}",
-                       "patches_per_level": {str(k): v.P for k, v in sim.levels.items()},
+                       "patches_per_level": ({str(k): int(len(v)) for k, v in sim.layout.items()}
+                                             if world > 1 else {str(k): v.P for k, v in sim.levels.items()}),
                        "cells_per_level": {str(k): v.ncells for k, v in sim.levels.items()},
-                       "parallelism": f"replica x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"SFC-sharded patches x{world} (NCCL shadow exchange)"
+                                       if world > 1 else "single GPU"),
                        "l2": (f"inputs larger than L2 (device state {pool_bytes / 1e9:.2f} GB)" if pool_bytes > 126e6 else f"device state {pool_bytes / 1e9:.3f} GB fits in L2 (no flush)"),
                        "dt_policy": "reference: level-1 stable_dt, r_t subcycling",
                        "host_ms_per_step": {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}},
