@@ -334,11 +334,12 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const int64_t FS = lv.field_stride;
     const int64_t base = pv.off + (int64_t)(tj0 + 1) * pv.NX + (ti0 + 1);
 
+    // density ratios rho_k / rho_m, only the k < m entries the sources use
     double rr[4][4];
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) rr[a][b] = (a < M && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
+        for (int b = 0; b < 4; ++b) rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
 
     // stage the padded tile with asynchronous 8-byte copies (LDGSTS): every
     // thread keeps ~3*(3M+1) global loads in flight instead of serialising
@@ -361,26 +362,6 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         sweep_tile<M, 1, true>(s, ny2, nx2, dt, lv.dy, prm, rr, best);
     else
         sweep_tile<M, 0, true>(s, ny2, nx2, dt, lv.dx, prm, rr, best);
-
-    // observed max speed of the pre-step interior
-    {
-        // block max (NaN-propagating); -1 marks "no wet column"
-        s.red[t] = best;
-        __syncthreads();
-        for (int st = NT / 2; st > 0; st >>= 1) {
-            if (t < st) {
-                const double a = s.red[t], b = s.red[t + st];
-                s.red[t] = (a < 0.0) ? b : ((b < 0.0) ? a : np_max(a, b));
-            }
-            __syncthreads();
-        }
-        if (t == 0 && !(s.red[0] < 0.0)) {
-            double v = s.red[0];
-            long long bits = (v != v) ? 0x7ff8000000000000LL : __double_as_longlong(v);
-            atomicMax(speed_bits + p, bits);
-        }
-        __syncthreads();
-    }
 
     if (YFIRST)
         sweep_tile<M, 0, false>(s, ny2, nx2, dt, lv.dx, prm, rr, best);
@@ -461,18 +442,46 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
             dst[(2 * M + m) * FS + gaddr] = hv[m];
         }
     })
-    // per-tile partials (fixed-order tree sums)
-    double *acc = tile_acc + (int64_t)tile * (M + 2);
+    // per-tile partials in one fused pass: warp shuffles (fixed xor tree),
+    // then warp 0 combines the NT/32 warp values in warp order -- the same
+    // order on every run, so the sums are deterministic
+    constexpr int NW = NT / 32;
+    const int lane = t & 31, warp = t >> 5;
+    double v[M + 2];
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-        const double sm = block_sum<NT>(negs[m], s.red);
-        if (t == 0) acc[m] = sm;
+    for (int m = 0; m < M; ++m) v[m] = negs[m];
+    v[M] = (double)fixes;
+    v[M + 1] = (double)repairs;
+    double sp = best;  // -1 = no wet column
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int q = 0; q < M + 2; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], off);
+        const double o = __shfl_xor_sync(0xffffffffu, sp, off);
+        sp = (sp < 0.0) ? o : ((o < 0.0) ? sp : np_max(sp, o));
     }
-    const long long fx = block_sum_ll<NT>(fixes, s.redi);
-    const long long rp = block_sum_ll<NT>(repairs, s.redi);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < M + 2; ++q) s.red[q * NW + warp] = v[q];
+        s.red[(M + 2) * NW + warp] = sp;
+    }
+    __syncthreads();
     if (t == 0) {
-        acc[M] = (double)fx;
-        acc[M + 1] = (double)rp;
+        double *acc = tile_acc + (int64_t)tile * (M + 2);
+        for (int q = 0; q < M + 2; ++q) {
+            double a = s.red[q * NW];
+            for (int w = 1; w < NW; ++w) a = a + s.red[q * NW + w];
+            acc[q] = a;
+        }
+        double b = s.red[(M + 2) * NW];
+        for (int w = 1; w < NW; ++w) {
+            const double o = s.red[(M + 2) * NW + w];
+            b = (b < 0.0) ? o : ((o < 0.0) ? b : np_max(b, o));
+        }
+        if (!(b < 0.0)) {
+            const long long bits = (b != b) ? 0x7ff8000000000000LL : __double_as_longlong(b);
+            atomicMax(speed_bits + p, bits);
+        }
     }
 }
 
