@@ -211,6 +211,12 @@ int mlamr_selftest_div(const double *a, const double *b, int n, unsigned long lo
 int mlamr_cluster_flags(const uint8_t *h_flags, int ny, int nx, double efficiency_target,
                         const uint8_t *h_allowed, int32_t *h_out_boxes, int max_boxes);
 
+/* The same clustering from summed-area tables built on the device: HOST
+ * int32 (ny+1) x (nx+1) tables of the flags and of the cells outside
+ * `allowed` (h_sat_bad NULL = all allowed), zero first row/column. */
+int mlamr_cluster_sat(const int32_t *h_sat_flags, const int32_t *h_sat_bad, int ny, int nx,
+                      double efficiency_target, int32_t *h_out_boxes, int max_boxes);
+
 /* Host-side max-patch-size chop of boxes (SURVEY.md App. B harness rule);
  * HOST int32 [n*4] in, HOST int32 [cap*4] out sorted by (lo_j, lo_i).
  * Returns the count or -1 when it exceeds cap. */

@@ -90,6 +90,8 @@ SIGNATURES = {
                                            ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_flags_reference": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              c_vp, c_vp, c_vp, c_vp]),
+    "mlamr_cluster_sat": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double, c_vp,
+                                         ctypes.c_int]),
     "mlamr_chop_boxes": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         c_vp, ctypes.c_int]),
     "mlamr_step_tile": (ctypes.c_int, [c_vp, c_vp]),

@@ -68,6 +68,12 @@ Cut signature_cut(const std::vector<int64_t> &sig) {
 struct Prefix {
     int ny = 0, nx = 0;
     std::vector<int32_t> *sat = nullptr;  // (ny+1) x (nx+1)
+    const int32_t *ext = nullptr;         // external table (device-built), same layout
+    void wrap(const int32_t *table, int ny_, int nx_) {
+        ny = ny_;
+        nx = nx_;
+        ext = table;
+    }
     void build(const uint8_t *m, int ny_, int nx_, std::vector<int32_t> &store) {
         ny = ny_;
         nx = nx_;
@@ -105,7 +111,7 @@ struct Prefix {
     }
     inline int64_t box(int i0, int j0, int i1, int j1) const {
         const size_t W = (size_t)nx + 1;
-        const int32_t *S = sat->data();
+        const int32_t *S = ext ? ext : sat->data();
         return (int64_t)S[(size_t)(j1 + 1) * W + i1 + 1] - S[(size_t)j0 * W + i1 + 1] -
                S[(size_t)(j1 + 1) * W + i0] + S[(size_t)j0 * W + i0];
     }
@@ -115,29 +121,9 @@ struct Prefix {
 
 }  // namespace
 
-// Returns the number of boxes written to out_boxes [n*4] as (lo_i, lo_j,
-// hi_i, hi_j) sorted by (lo_j, lo_i); -1 if more than max_boxes; -2 if a
-// flag lies outside `allowed` (the reference raises ValueError).
-extern "C" int mlamr_cluster_flags(const uint8_t *flags, int ny, int nx, double eff,
-                                   const uint8_t *allowed, int32_t *out_boxes, int max_boxes) {
-    static thread_local std::vector<int32_t> store_f, store_b;
-    static thread_local std::vector<uint8_t> bad;
-    Prefix F;
-    F.build(flags, ny, nx, store_f);
-    Prefix BAD;
-    if (allowed != nullptr) {
-        bad.resize((size_t)ny * nx);
-        uint8_t *badp = bad.data();  // thread_local storage: hand the pointer to the team
-        int outside = 0;
-        const int64_t n = (int64_t)ny * nx;
-#pragma omp parallel for schedule(static) reduction(|| : outside)
-        for (int64_t k = 0; k < n; ++k) {
-            badp[k] = allowed[k] ? 0 : 1;
-            outside = outside || (flags[k] && !allowed[k]);
-        }
-        if (outside) return -2;
-        BAD.build(bad.data(), ny, nx, store_b);
-    }
+static int cluster_recursion(const Prefix &F, const Prefix *BADp, int ny, int nx, double eff,
+                             int32_t *out_boxes, int max_boxes) {
+    const bool have_allowed = BADp != nullptr;
     struct Node { int i0, j0, i1, j1; };
     std::vector<Node> stack;
     std::vector<std::array<int, 4>> boxes;
@@ -155,7 +141,7 @@ extern "C" int mlamr_cluster_flags(const uint8_t *flags, int ny, int nx, double 
         const int64_t nflag = F.box(a_i, a_j, b_i, b_j);
         const int w = b_i - a_i + 1, h = b_j - a_j + 1;
         const int64_t area = (int64_t)w * h;
-        const bool ok = (allowed == nullptr) || BAD.box(a_i, a_j, b_i, b_j) == 0;
+        const bool ok = !have_allowed || BADp->box(a_i, a_j, b_i, b_j) == 0;
         if (area == 1 || (ok && (double)nflag >= eff * (double)area)) {
             boxes.push_back({a_i, a_j, b_i, b_j});
             continue;
@@ -188,6 +174,43 @@ extern "C" int mlamr_cluster_flags(const uint8_t *flags, int ny, int nx, double 
     for (size_t k = 0; k < boxes.size(); ++k)
         for (int q = 0; q < 4; ++q) out_boxes[4 * k + q] = boxes[k][q];
     return (int)boxes.size();
+}
+
+// Returns the number of boxes written to out_boxes [n*4] as (lo_i, lo_j,
+// hi_i, hi_j) sorted by (lo_j, lo_i); -1 if more than max_boxes; -2 if a
+// flag lies outside `allowed` (the reference raises ValueError).
+extern "C" int mlamr_cluster_flags(const uint8_t *flags, int ny, int nx, double eff,
+                                   const uint8_t *allowed, int32_t *out_boxes, int max_boxes) {
+    static thread_local std::vector<int32_t> store_f, store_b;
+    static thread_local std::vector<uint8_t> bad;
+    Prefix F;
+    F.build(flags, ny, nx, store_f);
+    Prefix BAD;
+    if (allowed != nullptr) {
+        bad.resize((size_t)ny * nx);
+        uint8_t *badp = bad.data();  // thread_local storage: hand the pointer to the team
+        int outside = 0;
+        const int64_t n = (int64_t)ny * nx;
+#pragma omp parallel for schedule(static) reduction(|| : outside)
+        for (int64_t k = 0; k < n; ++k) {
+            badp[k] = allowed[k] ? 0 : 1;
+            outside = outside || (flags[k] && !allowed[k]);
+        }
+        if (outside) return -2;
+        BAD.build(bad.data(), ny, nx, store_b);
+    }
+    return cluster_recursion(F, allowed != nullptr ? &BAD : nullptr, ny, nx, eff, out_boxes, max_boxes);
+}
+
+// Same clustering from summed-area tables built elsewhere (the device):
+// sat_flags / sat_bad are int32 (ny+1) x (nx+1), zero first row/column;
+// sat_bad counts cells outside `allowed` (NULL = everything allowed).
+extern "C" int mlamr_cluster_sat(const int32_t *sat_flags, const int32_t *sat_bad, int ny, int nx, double eff,
+                                 int32_t *out_boxes, int max_boxes) {
+    Prefix F, BAD;
+    F.wrap(sat_flags, ny, nx);
+    if (sat_bad != nullptr) BAD.wrap(sat_bad, ny, nx);
+    return cluster_recursion(F, sat_bad != nullptr ? &BAD : nullptr, ny, nx, eff, out_boxes, max_boxes);
 }
 
 // Harness max-patch-size chop of clustered boxes: each

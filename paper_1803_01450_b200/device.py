@@ -81,6 +81,7 @@ _ARENA = None
 # next pool instead of round-tripping GBs through cudaMalloc.  Reuse is
 # stream-ordered (everything runs on the driver's stream).
 _RECYCLE: list = []
+ALLOC_STATS = {"fresh": 0, "fresh_bytes": 0, "reused": 0}
 
 
 def acquire(numel: int, dtype, device, stream) -> torch.Tensor:
@@ -91,8 +92,11 @@ def acquire(numel: int, dtype, device, stream) -> torch.Tensor:
                 best = k
     if best is not None and _RECYCLE[best].numel() <= 3 * numel + (1 << 20):
         t = _RECYCLE.pop(best)
+        ALLOC_STATS["reused"] += 1
         return t[:numel]
     cap = int(numel * 1.5) + (1 << 16)
+    ALLOC_STATS["fresh"] += 1
+    ALLOC_STATS["fresh_bytes"] += cap * torch.tensor([], dtype=dtype).element_size()
     with torch.cuda.stream(stream):
         t = torch.empty(cap, dtype=dtype, device=device)
     return t[:numel]

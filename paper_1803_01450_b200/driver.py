@@ -38,7 +38,7 @@ from . import _native as N
 from .device import LevelPool, arena, empty_level_struct, paint_child_map, release
 from .errors import CflViolationError, NumericalAbortError, TimeSyncError, raise_status
 from .mesh import GHOST_WIDTH, IndexBox, LevelSpec, boxes_array, paint
-from .regrid import chop_boxes, cluster_boxes, nesting_allowed
+from .regrid import chop_boxes, cluster_boxes, cluster_boxes_device, nesting_allowed
 from .problems import gradient_flags_map
 
 _TIME_RTOL = 1e-12
@@ -259,15 +259,8 @@ class Simulation:
         rule = self.pb.flag_rule
         if rule[0] == "reference":
             b = self._flag_buffers(level)
+            self._device_flags(level)
             with torch.cuda.stream(self.stream):
-                b["bits"].zero_()
-                pl, nl = pool.work_list()
-                self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
-                           self._eta_rest.data_ptr(), self._wave_tol.data_ptr(), b["bits"].data_ptr(),
-                           pool.blocks_per_patch(pool.max_interior), pl, nl, self.sh)
-                self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
-                           self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
-                           b["scratch"].data_ptr(), self.sh)
                 b["flags_h"].copy_(b["flags"], non_blocking=True)
                 b["allowed_h"].copy_(b["allowed"], non_blocking=True)
             self.stream.synchronize()
@@ -292,6 +285,39 @@ class Simulation:
     def flags_for(self, level: int) -> np.ndarray:
         return self.flags_and_allowed(level)[0]
 
+    def _device_flags(self, level: int):
+        """Reference flag rule + nesting mask on the device (0/1 byte maps)."""
+        pool = self.levels[level]
+        s = self.spec(level)
+        b = self._flag_buffers(level)
+        with torch.cuda.stream(self.stream):
+            b["bits"].zero_()
+            pl, nl = pool.work_list()
+            if pool.P and (pl is None or nl > 0):
+                self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
+                           self._eta_rest.data_ptr(), self._wave_tol.data_ptr(), b["bits"].data_ptr(),
+                           pool.blocks_per_patch(pool.max_interior), pl, nl, self.sh)
+            self._reduce_flag_bits(b["bits"])
+            self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
+                       self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
+                       b["scratch"].data_ptr(), self.sh)
+        return b["flags"], b["allowed"]
+
+    def _reduce_flag_bits(self, bits) -> None:
+        """Single GPU: nothing to combine (the sharded driver all-reduces)."""
+
+    def _cluster_level(self, level: int) -> np.ndarray:
+        """Coarse boxes of the new finer level (cluster_flags, regrid.py:261)."""
+        s = self.spec(level)
+        if self.pb.flag_rule[0] == "reference":
+            flags_d, allowed_d = self._device_flags(level)
+            cb = cluster_boxes_device(flags_d, allowed_d, s.ny, s.nx, self.pb.efficiency_target, self.stream)
+            arena().reset()
+            self.d2h_bytes += 8 * (s.ny + 1) * (s.nx + 1)
+            return cb
+        flags, allowed = self.flags_and_allowed(level)
+        return cluster_boxes(flags, self.pb.efficiency_target, allowed)
+
     @staticmethod
     def _lexsorted(b: np.ndarray) -> np.ndarray:
         return b[np.lexsort((b[:, 0], b[:, 1]))] if len(b) else b
@@ -307,12 +333,10 @@ class Simulation:
             cb = np.stack([fb[:, 0] // rx, fb[:, 1] // ry, (fb[:, 2] + 1) // rx - 1, (fb[:, 3] + 1) // ry - 1], 1)
             cb = self._lexsorted(cb)
         else:
-            with self._timed("regrid.flags"):
-                flags, allowed = self.flags_and_allowed(level)
-            with self._timed("regrid.cluster"):
-                cb = cluster_boxes(flags, self.pb.efficiency_target, allowed)
-                if self.pb.max_patch is not None:
-                    cb = chop_boxes(cb, *self.pb.max_patch, aligned=self.pb.chop_aligned)
+            with self._timed("regrid.flags+cluster"):
+                cb = self._cluster_level(level)
+            if self.pb.max_patch is not None:
+                cb = chop_boxes(cb, *self.pb.max_patch, aligned=self.pb.chop_aligned)
         cb = np.asarray(cb, dtype=np.int64).reshape(-1, 4)
         nboxes = np.stack([cb[:, 0] * rx, cb[:, 1] * ry, (cb[:, 2] + 1) * rx - 1, (cb[:, 3] + 1) * ry - 1], 1)
         if old is not None:
@@ -320,8 +344,12 @@ class Simulation:
                 return False
         elif len(nboxes) == 0:
             return False
-        with self._timed("regrid.pool"):
-            new = self._new_pool(level + 1, nboxes)
+        from .device import ALLOC_STATS
+        f0 = ALLOC_STATS["fresh"]
+        t0p = time.perf_counter()
+        new = self._new_pool(level + 1, nboxes)
+        self.host_prof["regrid.pool(fresh alloc)" if ALLOC_STATS["fresh"] > f0 else "regrid.pool(reuse)"] += \
+            time.perf_counter() - t0p
         new.time = par.time
         M = self.M
         tq = time.perf_counter()

@@ -36,6 +36,38 @@ def cluster_boxes(flags: np.ndarray, efficiency_target: float, allowed=None) -> 
         cap *= 8
 
 
+_SAT_HOST = {}
+
+
+def cluster_boxes_device(flags_d, allowed_d, ny: int, nx: int, efficiency_target: float, stream):
+    """regrid.cluster_flags from device-resident 0/1 maps: the summed-area
+    tables are exact int32 cumulative sums on the GPU; only the bisection
+    recursion runs on the host (native C++)."""
+    import torch
+    key = (ny, nx)
+    if key not in _SAT_HOST:
+        _SAT_HOST[key] = (torch.empty((ny + 1) * (nx + 1), dtype=torch.int32, pin_memory=True),
+                          torch.empty((ny + 1) * (nx + 1), dtype=torch.int32, pin_memory=True))
+    hf, hb = _SAT_HOST[key]
+    with torch.cuda.stream(stream):
+        for src, host, invert in ((flags_d, hf, False), (allowed_d, hb, True)):
+            m = src.view(ny, nx).to(torch.int32)
+            if invert:
+                m = 1 - m
+            sat = torch.zeros((ny + 1, nx + 1), dtype=torch.int32, device=src.device)
+            sat[1:, 1:] = torch.cumsum(torch.cumsum(m, 0, dtype=torch.int32), 1, dtype=torch.int32)
+            host.copy_(sat.view(-1), non_blocking=True)
+    stream.synchronize()
+    cap = 4096
+    while True:
+        out = np.empty((cap, 4), dtype=np.int32)
+        n = N.lib().mlamr_cluster_sat(hf.data_ptr(), hb.data_ptr(), ny, nx, float(efficiency_target),
+                                      out.ctypes.data, cap)
+        if n >= 0:
+            return out[:n]
+        cap *= 8
+
+
 def chop_boxes(boxes: np.ndarray, max_nx: int, max_ny: int, aligned: bool = False) -> np.ndarray:
     """:func:`chop` in native C++ over an int32 [n, 4] array."""
     b = np.ascontiguousarray(boxes, dtype=np.int32).reshape(-1, 4)

@@ -189,9 +189,16 @@ class ShardedSimulation(Simulation):
         return st
 
     # -- flags over owned patches, all-reduced -----------------------------------------
+    def _reduce_flag_bits(self, bits) -> None:
+        """Each rank wrote the bits of its owned cells only: max == union."""
+        if self.world > 1:
+            wide = bits.to(torch.int32)
+            self.comm.allreduce(wide, dist.ReduceOp.MAX)
+            bits.copy_(wide.to(torch.uint8))
+
     def flags_and_allowed(self, level: int):
         s = self.spec(level)
-        if self.pb.flag_rule[0] != "reference":
+        if self.pb.flag_rule[0] == "bernoulli":
             from .mesh import dilate, paint
             from .regrid import nesting_allowed
             covered = paint(self.layout[level], s.ny, s.nx)
@@ -199,27 +206,7 @@ class ShardedSimulation(Simulation):
             f = dilate(f, self.pb.flag_rule[2]) & covered
             allowed = nesting_allowed(self.layout[level], s.ny, s.nx)
             return f & allowed, allowed
-        pool = self.levels[level]
-        b = self._flag_buffers(level)
-        with torch.cuda.stream(self.stream):
-            b["bits"].zero_()
-            pl, nl = pool.work_list()
-            if pool.P and (pl is None or nl > 0):
-                self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
-                           self._eta_rest.data_ptr(), self._wave_tol.data_ptr(), b["bits"].data_ptr(),
-                           pool.blocks_per_patch(pool.max_interior), pl, nl, self.sh)
-            if self.world > 1:
-                wide = b["bits"].to(torch.int32)
-                self.comm.allreduce(wide, dist.ReduceOp.MAX)
-                b["bits"].copy_(wide.to(torch.uint8))
-            self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
-                       self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
-                       b["scratch"].data_ptr(), self.sh)
-            b["flags_h"].copy_(b["flags"], non_blocking=True)
-            b["allowed_h"].copy_(b["allowed"], non_blocking=True)
-        self.stream.synchronize()
-        return (b["flags_h"].numpy().reshape(s.ny, s.nx).view(np.bool_),
-                b["allowed_h"].numpy().reshape(s.ny, s.nx).view(np.bool_))
+        return super().flags_and_allowed(level)
 
     # -- regrid --------------------------------------------------------------------------
     def _rebuild(self, level: int, init: bool = False) -> bool:
@@ -231,8 +218,7 @@ class ShardedSimulation(Simulation):
             cb = np.stack([fb[:, 0] // rx, fb[:, 1] // ry, (fb[:, 2] + 1) // rx - 1, (fb[:, 3] + 1) // ry - 1], 1)
             cb = self._lexsorted(cb)
         else:
-            flags, allowed = self.flags_and_allowed(level)
-            cb = cluster_boxes(flags, self.pb.efficiency_target, allowed)
+            cb = self._cluster_level(level)
             if self.pb.max_patch is not None:
                 cb = chop_boxes(cb, *self.pb.max_patch, aligned=self.pb.chop_aligned)
         cb = np.asarray(cb, dtype=np.int64).reshape(-1, 4)
