@@ -122,6 +122,22 @@ int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent,
                       mlamr_params prm, const int32_t *status,
                       const int32_t *patch_list, int n_list, void *stream);
 
+/* K2 as a per-layout plan + three lean kernels.  mlamr_ghost_plan writes,
+ * for every ghost cell of every patch (gbase = prefix sums of
+ * 4*(nx+4)+4*ny per patch), the element offset of the sibling interior
+ * cell covering it, -1 (in-domain, interpolate from the parent) or -2
+ * (outside the level box, boundary condition).  mlamr_fill_ghosts_planned
+ * then copies sibling cells, interpolates the compacted `interp_cells`
+ * (int32 pairs patch, ghost index) from the (blended) parent and applies
+ * the BCs of `bc_patches` -- the same values as mlamr_fill_ghosts. */
+int mlamr_ghost_plan(mlamr_level lv, const int64_t *gbase, int64_t *plan, int max_ghost, void *stream);
+int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *parent, const double *parent_old_state,
+                              double theta, int r_x, int r_y, const int32_t *bcs, mlamr_params prm,
+                              const int32_t *status, const int64_t *gbase, const int64_t *plan,
+                              const int32_t *patch_list, int n_list, int max_ghost,
+                              const int32_t *interp_cells, int n_interp,
+                              const int32_t *bc_patches, int n_bc, void *stream);
+
 /* Patch bathymetry (frame included) from a level-wide array of in-domain
  * values, then ghost.apply_bathymetry_bcs (ghost.py:118-129). */
 int mlamr_fill_bathymetry(mlamr_level lv, const double *level_bathy,

@@ -70,6 +70,11 @@ SIGNATURES = {
     "mlamr_fill_ghosts": (ctypes.c_int, [Level, ctypes.POINTER(Level), c_vp, ctypes.c_double,
                                          ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp,
                                          ctypes.c_int, c_vp]),
+    "mlamr_ghost_plan": (ctypes.c_int, [Level, c_vp, c_vp, ctypes.c_int, c_vp]),
+    "mlamr_fill_ghosts_planned": (ctypes.c_int, [Level, ctypes.POINTER(Level), c_vp, ctypes.c_double,
+                                                 ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp, c_vp,
+                                                 c_vp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, c_vp,
+                                                 ctypes.c_int, c_vp]),
     "mlamr_fill_bathymetry": (ctypes.c_int, [Level, c_vp, c_i32p, c_vp]),
     "mlamr_average_down": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, Params, c_vp,
                                           ctypes.c_int, c_vp, c_vp]),

@@ -172,6 +172,108 @@ __global__ void __launch_bounds__(NTA) k_fill_ghosts(mlamr_level lv, mlamr_level
     apply_bcs<M>(lv, pv, bcs, nullptr);
 }
 
+// ---------------------------------------------------------------------------
+// K2 split into a per-layout plan and three lean kernels.
+// Ghost cells of patch p are enumerated 0..nghost(p)-1 exactly as
+// ghost_cell_of(); gbase[p] is the prefix sum of nghost over the pool.
+// plan[gbase[p] + idx] = element offset of the sibling cell that covers it
+// (interior owner, ghost.py:186-196), -1 = in-domain but no sibling
+// (coarse interpolation, ghost.py:167-185), -2 = outside the level box
+// (physical BC, ghost.py:132-142).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(NTA) k_ghost_plan(mlamr_level lv, const int64_t *gbase, int64_t *plan) {
+    const int p = blockIdx.y;
+    const PatchView pv = patch_view(lv, p);
+    const int nghost = 4 * pv.NX + 4 * pv.ny;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nghost; idx += gridDim.x * NTA) {
+        int J, I;
+        ghost_cell_of(idx, pv.NX, pv.NY, pv.ny, J, I);
+        const int gi = pv.lo_i - MLAMR_G + I, gj = pv.lo_j - MLAMR_G + J;
+        int64_t v;
+        if (gi < 0 || gj < 0 || gi >= lv.level_nx || gj >= lv.level_ny) {
+            v = -2;
+        } else {
+            const int sib = owner_at(lv.own, lv.level_nx, lv.level_ny, gi, gj);
+            if (sib >= 0 && sib != p) {
+                const int32_t *b = lv.box + 4 * sib;
+                const int SNX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+                v = lv.offset[sib] + (int64_t)(gj - b[1] + MLAMR_G) * SNX + (gi - b[0] + MLAMR_G);
+            } else {
+                v = -1;
+            }
+        }
+        plan[gbase[p] + idx] = v;
+    }
+}
+
+// sibling copies: one thread per (ghost cell, patch); a single plan load
+// precedes the 3M independent loads.
+template <int M>
+__global__ void __launch_bounds__(NTA) k_fill_copy(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
+                                                   const int32_t *plist, const int32_t *status) {
+    if (status != nullptr && *status != 0) return;
+    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+    const int32_t *b = lv.box + 4 * p;
+    const int NX = b[2] - b[0] + 1 + 2 * MLAMR_G, ny = b[3] - b[1] + 1;
+    const int nghost = 4 * NX + 4 * ny;
+    const int64_t FS = lv.field_stride;
+    const int64_t off = lv.offset[p];
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nghost; idx += gridDim.x * NTA) {
+        const int64_t src = plan[gbase[p] + idx];
+        if (src < 0) continue;
+        int J, I;
+        ghost_cell_of(idx, NX, ny + 2 * MLAMR_G, ny, J, I);
+        const int64_t k = off + (int64_t)J * NX + I;
+        double v[3 * M];
+#pragma unroll
+        for (int q = 0; q < 3 * M; ++q) v[q] = lv.state[q * FS + src];
+#pragma unroll
+        for (int q = 0; q < 3 * M; ++q) lv.state[q * FS + k] = v[q];
+    }
+}
+
+// coarse interpolation of the cells of a compacted list (patch, ghost idx)
+template <int M>
+__global__ void __launch_bounds__(NTA) k_fill_interp(mlamr_level lv, mlamr_level par, const double *par_old,
+                                                     double theta, int r_x, int r_y, const int32_t *cells,
+                                                     int n_cells, mlamr_params prm, const int32_t *status) {
+    if (status != nullptr && *status != 0) return;
+    const double tol = prm.dry_tolerance;
+    const int64_t FS = lv.field_stride;
+    for (int c = blockIdx.x * NTA + threadIdx.x; c < n_cells; c += gridDim.x * NTA) {
+        const int p = cells[2 * c], idx = cells[2 * c + 1];
+        const int32_t *b = lv.box + 4 * p;
+        const int NX = b[2] - b[0] + 1 + 2 * MLAMR_G, ny = b[3] - b[1] + 1;
+        int J, I;
+        ghost_cell_of(idx, NX, ny + 2 * MLAMR_G, ny, J, I);
+        const int gi = b[0] - MLAMR_G + I, gj = b[1] - MLAMR_G + J;
+        const int64_t k = lv.offset[p] + (int64_t)J * NX + I;
+        const int pi = floordiv(gi, r_x), pj = floordiv(gj, r_y);
+        Coarse5<M> cc;
+        gather5<M>(par, par.state, par_old, theta, true, pi, pj, cc);
+        Slopes<M> sl;
+        parent_slopes<M>(cc, tol, sl);
+        double h[M], hu[M], hv[M];
+        fine_cell<M>(sl, child_offset(gi, pi, r_x), child_offset(gj, pj, r_y), lv.bathy[k], tol, h, hu, hv);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            lv.state[m * FS + k] = h[m];
+            lv.state[(M + m) * FS + k] = hu[m];
+            lv.state[(2 * M + m) * FS + k] = hv[m];
+        }
+    }
+}
+
+// physical BCs of the patches touching the level box (block per patch)
+template <int M>
+__global__ void __launch_bounds__(NTA) k_fill_bc(mlamr_level lv, const int32_t *plist, int4 bcs,
+                                                 const int32_t *status) {
+    if (status != nullptr && *status != 0) return;
+    const int p = plist[blockIdx.x];
+    const PatchView pv = patch_view(lv, p);
+    apply_bcs<M>(lv, pv, bcs, nullptr);
+}
+
 __global__ void __launch_bounds__(NTA) k_fill_bathy(mlamr_level lv, const double *level_bathy, int4 bcs) {
     const int p = blockIdx.x;
     const PatchView pv = patch_view(lv, p);
@@ -606,6 +708,40 @@ extern "C" int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent, cons
         constexpr int M = decltype(Mc)::value;
         k_fill_ghosts<M><<<nb, NTA, 0, st>>>(lv, par, parent != nullptr, parent_old_state, theta,
                                              r_x, r_y, b, prm, status, patch_list);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_ghost_plan(mlamr_level lv, const int64_t *gbase, int64_t *plan, int max_ghost,
+                                void *stream) {
+    if (lv.num_patches <= 0) return 0;
+    dim3 grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), (unsigned)lv.num_patches);
+    k_ghost_plan<<<grid, NTA, 0, as_stream(stream)>>>(lv, gbase, plan);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *parent, const double *parent_old_state,
+                                         double theta, int r_x, int r_y, const int32_t *bcs, mlamr_params prm,
+                                         const int32_t *status, const int64_t *gbase, const int64_t *plan,
+                                         const int32_t *patch_list, int n_list, int max_ghost,
+                                         const int32_t *interp_cells, int n_interp,
+                                         const int32_t *bc_patches, int n_bc, void *stream) {
+    const int nb = patch_list ? n_list : lv.num_patches;
+    cudaStream_t st = as_stream(stream);
+    const int4 b = make_int4(bcs[0], bcs[1], bcs[2], bcs[3]);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        if (nb > 0) {
+            dim3 grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), (unsigned)nb);
+            k_fill_copy<M><<<grid, NTA, 0, st>>>(lv, gbase, plan, patch_list, status);
+        }
+        if (parent != nullptr && n_interp > 0) {
+            const int blocks = (int)std::min<int64_t>((n_interp + NTA - 1) / NTA, 148 * 32);
+            k_fill_interp<M><<<blocks, NTA, 0, st>>>(lv, *parent, parent_old_state, theta, r_x, r_y,
+                                                     interp_cells, n_interp, prm, status);
+        }
+        if (n_bc > 0) k_fill_bc<M><<<n_bc, NTA, 0, st>>>(lv, bc_patches, b, status);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();

@@ -241,6 +241,42 @@ class LevelPool:
         lv.gown = self.gown.data_ptr() if self.gown is not None else None
         return lv
 
+    def ghost_plan(self):
+        """Per-layout K2 plan (mlamr_ghost_plan): sibling source of every ghost
+        cell, the compacted list of cells to interpolate from the parent, and
+        the patches that need physical BCs -- restricted to owned patches."""
+        if getattr(self, "_plan", None) is not None:
+            return self._plan
+        b = self.boxes
+        nx = b[:, 2] - b[:, 0] + 1
+        ny = b[:, 3] - b[:, 1] + 1
+        ng = 4 * (nx + 2 * GHOST_WIDTH) + 4 * ny
+        gbase = np.concatenate([[0], np.cumsum(ng)[:-1]]).astype(np.int64)
+        total = int(ng.sum())
+        A = arena()
+        with torch.cuda.stream(self.stream):
+            gbase_d = A.upload(gbase, self.device, self.stream)
+            plan = torch.empty(max(total, 1), dtype=torch.int64, device=self.device)
+            N.check(N.lib().mlamr_ghost_plan(self.struct(), gbase_d.data_ptr(), plan.data_ptr(), int(ng.max()),
+                                             self.stream.cuda_stream), "ghost_plan")
+            sel = plan[:total] == -1
+            if self.owned is not None:
+                own_cells = torch.repeat_interleave(torch.from_numpy(self.owned).to(self.device),
+                                                    torch.from_numpy(ng).to(self.device))
+                sel &= own_cells
+            gidx = torch.nonzero(sel).flatten()
+            patch = torch.searchsorted(gbase_d, gidx, right=True) - 1
+            cells = torch.stack([patch, gidx - gbase_d[patch]], dim=1).to(torch.int32).contiguous()
+        s = self.spec
+        touch = (b[:, 0] == 0) | (b[:, 2] == s.nx - 1) | (b[:, 1] == 0) | (b[:, 3] == s.ny - 1)
+        if self.owned is not None:
+            touch &= self.owned
+        bcp = np.flatnonzero(touch).astype(np.int32)
+        bc_d = A.upload(bcp, self.device, self.stream) if len(bcp) else torch.zeros(1, dtype=torch.int32,
+                                                                                     device=self.device)
+        self._plan = (gbase_d, plan, cells, int(cells.shape[0]), bc_d, len(bcp), int(ng.max()) if len(ng) else 0)
+        return self._plan
+
     def work_list(self):
         """(device patch-list pointer, count) of the patches this rank owns,
         or (None, 0) when it owns them all (single-GPU runs)."""

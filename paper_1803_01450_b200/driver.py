@@ -211,8 +211,10 @@ class Simulation:
                 theta = min(1.0, max(0.0, (t - t0) / dt)) if dt > 0 else 1.0
                 old_ptr = old.data_ptr()
         pl, nl = pool.work_list()
-        self._call(self.lib.mlamr_fill_ghosts, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
-                   self.prm, self.status.data_ptr(), pl, nl, self.sh)
+        gbase, plan, cells, n_cells, bc_d, n_bc, max_ghost = pool.ghost_plan()
+        self._call(self.lib.mlamr_fill_ghosts_planned, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
+                   self.prm, self.status.data_ptr(), gbase.data_ptr(), plan.data_ptr(), pl, nl, max_ghost,
+                   cells.data_ptr(), n_cells, bc_d.data_ptr(), n_bc, self.sh)
         pool.ghosts_in_cur = True
 
     # -- regridding (driver.py:192-222, regrid.py:235-353) -------------------------
