@@ -18,16 +18,18 @@
 // reference (which does not contract either).
 
 #include <cstdio>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
 namespace mlamr {
 
 #ifndef MLAMR_STEP_TY
-#define MLAMR_STEP_TY 16
+#define MLAMR_STEP_TY 8
 #endif
 #ifndef MLAMR_STEP_MINB
-#define MLAMR_STEP_MINB 1
+#define MLAMR_STEP_MINB 4
 #endif
 constexpr int TX = 32;
 constexpr int TY = MLAMR_STEP_TY;
@@ -539,7 +541,12 @@ __global__ void __launch_bounds__(NT) k_max_speed(mlamr_level lv, const double *
     }
 }
 
-// CFL guard + deterministic reduction of the step partials.
+// CFL guard + deterministic reduction of the step partials.  FIN_BLOCKS
+// CTAs each reduce a fixed contiguous chunk of tiles into chunk[b][q]; the
+// last CTA to finish (atomic ticket) sums the chunks in order and applies
+// the CFL guard, so the result is independent of scheduling.
+constexpr int FIN_BLOCKS = 148;
+
 template <int M>
 __global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const double *__restrict__ src,
                                                       double *__restrict__ dst,
@@ -547,20 +554,36 @@ __global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const doub
                                                       int n_tiles, double dt,
                                                       const long long *speed_bits,
                                                       const double *tile_acc, double *acc,
-                                                      int32_t *status, int32_t *bad_patch) {
+                                                      int32_t *status, int32_t *bad_patch,
+                                                      double *chunk, unsigned int *ticket) {
     __shared__ double red[NT];
     __shared__ int viol;
+    __shared__ bool last;
     const int t = threadIdx.x;
     if (*status != 0) return;
     const int K = M + 2;
-    const double area = lv.dx * lv.dy;
+    const int per = (n_tiles + FIN_BLOCKS - 1) / FIN_BLOCKS;
+    const int t0 = blockIdx.x * per, t1 = min(n_tiles, t0 + per);
     for (int q = 0; q < K; ++q) {
         double v = 0.0;
-        for (int i = t; i < n_tiles; i += NT) v = v + tile_acc[(int64_t)i * K + q];
+        for (int i = t0 + t; i < t1; i += NT) v = v + tile_acc[(int64_t)i * K + q];
         const double sm = block_sum<NT>(v, red);
-        // clipped mass = -(sum of negative depths) * cell area (physics.py:360-362)
-        if (t == 0) acc[q] = acc[q] + (q < M ? (-sm) * area : sm);
+        if (t == 0) chunk[blockIdx.x * K + q] = sm;
     }
+    __threadfence();
+    __syncthreads();
+    if (t == 0) last = (atomicAdd(ticket, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const double area = lv.dx * lv.dy;
+    if (t < K) {
+        double sm = 0.0;
+        for (int b2 = 0; b2 < (int)gridDim.x; ++b2) sm = sm + ((volatile double *)chunk)[b2 * K + t];
+        // clipped mass = -(sum of negative depths) * cell area (physics.py:360-362)
+        acc[t] = acc[t] + (t < M ? (-sm) * area : sm);
+    }
+    if (t == 0) *ticket = 0u;
     const double dmin = lv.dx < lv.dy ? lv.dx : lv.dy;
     if (t == 0) viol = 0;
     __syncthreads();
@@ -646,10 +669,32 @@ extern "C" int mlamr_step_finalize(mlamr_level lv, const double *src_state, doub
                                    const double *tile_acc, double *acc, int32_t *status,
                                    int32_t *bad_patch, void *stream) {
     cudaStream_t st = as_stream(stream);
+    // scratch for the chunk sums and the completion ticket, one per
+    // (device, stream): launches on one stream are ordered, so reuse is safe
+    struct Scratch { double *chunk; unsigned int *ticket; };
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, Scratch> pool;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Scratch sc;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = pool.find({dev, st});
+        if (it == pool.end()) {
+            if (cudaMalloc(&sc.chunk, sizeof(double) * FIN_BLOCKS * (MLAMR_MAX_LAYERS + 2)) != cudaSuccess) return -2;
+            if (cudaMalloc(&sc.ticket, sizeof(unsigned int)) != cudaSuccess) return -2;
+            cudaMemsetAsync(sc.ticket, 0, sizeof(unsigned int), st);
+            pool[{dev, st}] = sc;
+        } else {
+            sc = it->second;
+        }
+    }
+    double *chunk = sc.chunk;
+    unsigned int *ticket = sc.ticket;
     switch (prm.num_layers) {
-        case 1: k_step_finalize<1><<<1, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch); break;
-        case 2: k_step_finalize<2><<<1, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch); break;
-        case 3: k_step_finalize<3><<<1, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch); break;
+        case 1: k_step_finalize<1><<<FIN_BLOCKS, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
+        case 2: k_step_finalize<2><<<FIN_BLOCKS, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
+        case 3: k_step_finalize<3><<<FIN_BLOCKS, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
         default: return -1;
     }
     return (int)cudaGetLastError();
