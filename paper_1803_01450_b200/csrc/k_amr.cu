@@ -293,41 +293,61 @@ __global__ void __launch_bounds__(NTA) k_fill_bathy(mlamr_level lv, const double
 // K4: coarsening (coarsen.average_down, coarsen.py:30-76)
 // One thread per coarse cell of a fine patch's footprint.
 // ---------------------------------------------------------------------------
-template <int M>
-__global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_level coarse, int r_x,
-                                                      int r_y, mlamr_params prm, double *patch_delta,
+// RX/RY > 0: compile-time ratios (fully unrolled, all loads in flight);
+// 0: runtime ratios.  Same summation order either way (coarsen.py:21-27).
+template <int M, int RX, int RY>
+__global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_level coarse, int r_x_, int r_y_,
+                                                      mlamr_params prm, double *patch_delta,
                                                       const int32_t *status) {
     __shared__ double red[NTA];
     if (status != nullptr && *status != 0) return;
+    const int r_x = RX > 0 ? RX : r_x_;
+    const int r_y = RY > 0 ? RY : r_y_;
     const int p = blockIdx.y;
     const PatchView fv = patch_view(fine, p);
     const int cnx = fv.nx / r_x, cny = fv.ny / r_y;
     const int clo_i = floordiv(fv.lo_i, r_x), clo_j = floordiv(fv.lo_j, r_y);
     const int64_t FF = fine.field_stride, CF = coarse.field_stride;
     const double tol = prm.dry_tolerance;
-    const double inv_n = (double)(r_x * r_y);
+    const double nblk = (double)(r_x * r_y);
     double dsum[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) dsum[m] = 0.0;
     for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
-        const int J = idx / cnx, I = idx % cnx;
+        const int J = idx / cnx, I = idx - (idx / cnx) * cnx;
         const int ci = clo_i + I, cj = clo_j + J;
         const int o = owner_at(coarse.own, coarse.level_nx, coarse.level_ny, ci, cj);
         if (o < 0) continue;
+        const int64_t base = fv.off + (int64_t)(MLAMR_G + J * r_y) * fv.NX + (MLAMR_G + I * r_x);
         double avg[3][M];
 #pragma unroll
         for (int f = 0; f < 3; ++f)
 #pragma unroll
             for (int m = 0; m < M; ++m) {
-                const double *a = fine.state + (f * M + m) * FF + fv.off;
+                const double *a = fine.state + (f * M + m) * FF + base;
                 double s = 0.0;
-                for (int q = 0; q < r_y; ++q) {
-                    const double *row = a + (int64_t)(MLAMR_G + J * r_y + q) * fv.NX + (MLAMR_G + I * r_x);
-                    double rs = row[0];
-                    for (int pp = 1; pp < r_x; ++pp) rs = rs + row[pp];
-                    s = (q == 0) ? rs : s + rs;
+                if (RX > 0 && RY > 0) {
+                    double v[RY > 0 ? RY : 1][RX > 0 ? RX : 1];
+#pragma unroll
+                    for (int q = 0; q < (RY > 0 ? RY : 1); ++q)
+#pragma unroll
+                        for (int pp = 0; pp < (RX > 0 ? RX : 1); ++pp) v[q][pp] = a[(int64_t)q * fv.NX + pp];
+#pragma unroll
+                    for (int q = 0; q < (RY > 0 ? RY : 1); ++q) {
+                        double rs = v[q][0];
+#pragma unroll
+                        for (int pp = 1; pp < (RX > 0 ? RX : 1); ++pp) rs = rs + v[q][pp];
+                        s = (q == 0) ? rs : s + rs;
+                    }
+                } else {
+                    for (int q = 0; q < r_y; ++q) {
+                        const double *row = a + (int64_t)q * fv.NX;
+                        double rs = row[0];
+                        for (int pp = 1; pp < r_x; ++pp) rs = rs + row[pp];
+                        s = (q == 0) ? rs : s + rs;
+                    }
                 }
-                avg[f][m] = s / inv_n;
+                avg[f][m] = s / nblk;
             }
         const int32_t *b = coarse.box + 4 * o;
         const int CNX = b[2] - b[0] + 1 + 2 * MLAMR_G;
@@ -763,7 +783,14 @@ extern "C" int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x,
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_average_down<M><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
+        if (r_x == 4 && r_y == 4)
+            k_average_down<M, 4, 4><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
+        else if (r_x == 2 && r_y == 2)
+            k_average_down<M, 2, 2><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
+        else if (r_x == 4 && r_y == 2)
+            k_average_down<M, 4, 2><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
+        else
+            k_average_down<M, 0, 0><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
