@@ -88,12 +88,12 @@ __device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
 // DIR 0 = x (interfaces between columns c, c+1), 1 = y (rows r, r+1).
 // FIRST: all halo lines (the reference's full=True); else interior lines.
 template <int M, int DIR, bool FIRST>
-__device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d,
+__device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
                            const mlamr_params &prm, const double (&rr)[4][4], double &best) {
+    // lam = dt / d and yd = recip_nr(d) come from the kernel prologue, where
+    // their latency overlaps the tile's in-flight loads
     const double g = prm.gravity;
     const double tol = prm.dry_tolerance;
-    const double lam = dt / d;
-    const double yd = recip_nr(d);
     const double *B = s.S[3 * M];
     constexpr int STEP = DIR == 0 ? 1 : PX;  // neighbour offset along the sweep
     const int n_along = DIR == 0 ? nx2 : ny2;
@@ -336,13 +336,6 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const int64_t FS = lv.field_stride;
     const int64_t base = pv.off + (int64_t)(tj0 + 1) * pv.NX + (ti0 + 1);
 
-    // density ratios rho_k / rho_m, only the k < m entries the sources use
-    double rr[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
-
     // stage the padded tile with asynchronous 8-byte copies (LDGSTS): every
     // thread keeps ~3*(3M+1) global loads in flight instead of serialising
     // load -> shared store pairs
@@ -356,19 +349,28 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         })
     }
     asm volatile("cp.async.commit_group;\n" ::);
+    // density ratios rho_k / rho_m, only the k < m entries the sources use
+    double rr[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
+
+    const double lam_x = dt / lv.dx, lam_y = dt / lv.dy;
+    const double y_x = recip_nr(lv.dx), y_y = recip_nr(lv.dy);
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
 
     double best = -1.0;  // running observed speed over this thread's cells
     if (YFIRST)
-        sweep_tile<M, 1, true>(s, ny2, nx2, dt, lv.dy, prm, rr, best);
+        sweep_tile<M, 1, true>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
     else
-        sweep_tile<M, 0, true>(s, ny2, nx2, dt, lv.dx, prm, rr, best);
+        sweep_tile<M, 0, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
 
     if (YFIRST)
-        sweep_tile<M, 0, false>(s, ny2, nx2, dt, lv.dx, prm, rr, best);
+        sweep_tile<M, 0, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
     else
-        sweep_tile<M, 1, false>(s, ny2, nx2, dt, lv.dy, prm, rr, best);
+        sweep_tile<M, 1, false>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
 
     // post-processing on the tile interior (physics.py:360-376)
     const double tol = prm.dry_tolerance;
