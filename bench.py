@@ -247,6 +247,13 @@ def b200_arm(args):
         durs.append(a.elapsed_time(b) * 1e-3)
         byts.append(step_bytes(pool, M))
     peak, peak_kind = _peaks()
+    traffic, traffic_ratio = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "step_traffic.json")) as f:
+            tj = json.load(f)
+        traffic, traffic_ratio = tj["dram_bytes"], tj["traffic_over_algorithmic"]
+    except Exception:
+        pass
     achieved = (sum(byts) / sum(durs)) / 1e9 if durs else None
     step_share = sum(durs) / (ms * 1e-3) if durs else None
     sim.step_timer_level = None
@@ -307,7 +314,10 @@ def b200_arm(args):
                        "dt_policy": "reference: level-1 stable_dt, r_t subcycling",
                        "host_ms_per_step": {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_over_algorithmic": traffic_ratio,
+                         "traffic_source": "ncu --set full capture of one C4 level-3 launch "
+                                           "(profiles/r01/step_traffic.json)",
                          "kernel": "mlamr_step (k_step) on the finest level",
                          "bytes_per_launch": int(np.mean(byts)) if byts else None,
                          "avg_launch_ms": 1e3 * float(np.mean(durs)) if durs else None,

@@ -42,6 +42,7 @@ from .regrid import chop_boxes, cluster_boxes, cluster_boxes_device, nesting_all
 from .problems import gradient_flags_map
 
 _TIME_RTOL = 1e-12
+_LOG_STEP_BYTES = bool(__import__("os").environ.get("MLAMR_LOG_STEP_BYTES"))
 
 
 @dataclass
@@ -412,6 +413,12 @@ class Simulation:
             pool.speed_bits.fill_(-1)
         src, dst = pool.state, pool.other
         lv = pool.struct(src)
+        if _LOG_STEP_BYTES:
+            b = pool.boxes if pool.owned is None else pool.boxes[pool.owned]
+            nx, ny = b[:, 2] - b[:, 0] + 1, b[:, 3] - b[:, 1] + 1
+            byts = int((8 * ((3 * self.M + 1) * (nx + 2) * (ny + 2) + 3 * self.M * nx * ny)).sum())
+            import sys
+            print(f"[mlamr] step level={level} tiles={pool.n_tiles} algorithmic_bytes={byts}", file=sys.stderr)
         timed = self.step_timer_level == level
         if timed:
             e0 = torch.cuda.Event(enable_timing=True)
