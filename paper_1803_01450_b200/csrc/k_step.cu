@@ -26,18 +26,25 @@
 namespace mlamr {
 
 #ifndef MLAMR_STEP_TY
-#define MLAMR_STEP_TY 8
+#define MLAMR_STEP_TY 16
 #endif
 #ifndef MLAMR_STEP_MINB
-#define MLAMR_STEP_MINB 4
+#define MLAMR_STEP_MINB 2
 #endif
-constexpr int TX = 32;
+#ifndef MLAMR_STEP_TX
+#define MLAMR_STEP_TX 32
+#endif
+#ifndef MLAMR_STEP_NT
+#define MLAMR_STEP_NT 320
+#endif
+constexpr int TX = MLAMR_STEP_TX;
 constexpr int TY = MLAMR_STEP_TY;
 constexpr int PX = TX + 2;
 constexpr int PY = TY + 2;
 constexpr int NPAD = PX * PY;
 constexpr int NFLUX = PY * PX;  // interface (r,c) stored at the cell index of its left/lower cell
-constexpr int NT = 256;
+constexpr int NT = MLAMR_STEP_NT;  // threads of the step CTA
+constexpr int NTF = 256;           // threads of the helper kernels (power of two)
 
 template <int M>
 struct StepSmem {
@@ -337,16 +344,33 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const int64_t base = pv.off + (int64_t)(tj0 + 1) * pv.NX + (ti0 + 1);
 
     // stage the padded tile with asynchronous 8-byte copies (LDGSTS): every
-    // thread keeps ~3*(3M+1) global loads in flight instead of serialising
-    // load -> shared store pairs
-#pragma unroll 1
-    for (int q = 0; q < 3 * M + 1; ++q) {
-        const double *g = (q < 3 * M) ? src + q * FS : lv.bathy;
-        FOR_RECT(0, ny2, 0, nx2, {
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(&s.S[q][r * PX + c]);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
-                         "l"(g + base + (int64_t)r * pv.NX + c));
-        })
+    // thread keeps ~NITEM*(3M+1) global loads in flight instead of
+    // serialising load -> shared store pairs.  The (row, column) split of a
+    // thread's items is done once; each plane then costs one address add and
+    // one LDGSTS per item.
+    {
+        constexpr int NITEM = (NPAD + NT - 1) / NT;
+        unsigned sa[NITEM];
+        const double *ga[NITEM];
+        bool in[NITEM];
+#pragma unroll
+        for (int i = 0; i < NITEM; ++i) {
+            const int idx = t + i * NT;
+            const int r = idx / PX, c = idx - (idx / PX) * PX;
+            in[i] = idx < ny2 * PX && c < nx2;
+            sa[i] = (unsigned)__cvta_generic_to_shared(&s.S[0][0]) + idx * 8;
+            ga[i] = src + base + (int64_t)r * pv.NX + c;
+        }
+        const int64_t boff = lv.bathy - src;  // same patch layout, one plane
+#pragma unroll
+        for (int q = 0; q < 3 * M + 1; ++q) {
+            const int64_t po = (q < 3 * M) ? q * FS : boff;
+#pragma unroll
+            for (int i = 0; i < NITEM; ++i)
+                if (in[i])
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa[i] + q * NPAD * 8),
+                                 "l"(ga[i] + po));
+        }
     }
     asm volatile("cp.async.commit_group;\n" ::);
     // density ratios rho_k / rho_m, only the k < m entries the sources use
@@ -456,18 +480,32 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     for (int m = 0; m < M; ++m) v[m] = negs[m];
     v[M] = (double)fixes;
     v[M + 1] = (double)repairs;
-    double sp = best;  // -1 = no wet column
+    // negative-depth sums and counters are zero in almost every warp: the
+    // shuffle tree runs only where one is not
+    bool any = false;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
+    for (int q = 0; q < M + 2; ++q) any = any || (v[q] != 0.0);
+    if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
-        for (int q = 0; q < M + 2; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], off);
-        const double o = __shfl_xor_sync(0xffffffffu, sp, off);
-        sp = (sp < 0.0) ? o : ((o < 0.0) ? sp : np_max(sp, o));
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int q = 0; q < M + 2; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], off);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < M + 2; ++q) v[q] = 0.0;
     }
+    // speed max on the bit patterns: speeds are >= 0 (or NaN, canonicalised
+    // above every finite value), and "no wet column" is -1, so the ordering
+    // of the signed 64-bit patterns is the numpy maximum the reference takes
+    const long long mybits = (best < 0.0) ? -1LL
+                           : ((best != best) ? 0x7ff8000000000000LL : __double_as_longlong(best));
+    const int hi = __reduce_max_sync(0xffffffffu, (int)(mybits >> 32));
+    const unsigned lo = __reduce_max_sync(0xffffffffu, ((int)(mybits >> 32) == hi) ? (unsigned)mybits : 0u);
     if (lane == 0) {
 #pragma unroll
         for (int q = 0; q < M + 2; ++q) s.red[q * NW + warp] = v[q];
-        s.red[(M + 2) * NW + warp] = sp;
+        s.redi[warp] = (hi < 0) ? -1LL : (long long)(((unsigned long long)(unsigned)hi << 32) | lo);
     }
     __syncthreads();
     if (t == 0) {
@@ -477,24 +515,18 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
             for (int w = 1; w < NW; ++w) a = a + s.red[q * NW + w];
             acc[q] = a;
         }
-        double b = s.red[(M + 2) * NW];
-        for (int w = 1; w < NW; ++w) {
-            const double o = s.red[(M + 2) * NW + w];
-            b = (b < 0.0) ? o : ((o < 0.0) ? b : np_max(b, o));
-        }
-        if (!(b < 0.0)) {
-            const long long bits = (b != b) ? 0x7ff8000000000000LL : __double_as_longlong(b);
-            atomicMax(speed_bits + p, bits);
-        }
+        long long b = s.redi[0];
+        for (int w = 1; w < NW; ++w) b = max(b, s.redi[w]);
+        if (b >= 0) atomicMax(speed_bits + p, b);
     }
 }
 
 // K6: observed max speed per patch without stepping (stable_dt, level 1 dt).
 template <int M>
-__global__ void __launch_bounds__(NT) k_max_speed(mlamr_level lv, const double *__restrict__ st,
+__global__ void __launch_bounds__(NTF) k_max_speed(mlamr_level lv, const double *__restrict__ st,
                                                   const int32_t *__restrict__ tiles,
                                                   mlamr_params prm, long long *speed_bits) {
-    __shared__ double red[NT];
+    __shared__ double red[NTF];
     const int t = threadIdx.x;
     const int tile = blockIdx.x;
     const int p = tiles[3 * tile];
@@ -507,7 +539,7 @@ __global__ void __launch_bounds__(NT) k_max_speed(mlamr_level lv, const double *
     const double tol = prm.dry_tolerance;
     double best = -1.0;
     bool any = false;
-    for (int idx = t; idx < ty * tx; idx += NT) {
+    for (int idx = t; idx < ty * tx; idx += NTF) {
         const int r = idx / tx;
         const int c = idx - r * tx;
         const int64_t k = pv.off + (int64_t)(tj0 + MLAMR_G + r) * pv.NX + (ti0 + MLAMR_G + c);
@@ -529,7 +561,7 @@ __global__ void __launch_bounds__(NT) k_max_speed(mlamr_level lv, const double *
     }
     red[t] = any ? best : -1.0;
     __syncthreads();
-    for (int s2 = NT / 2; s2 > 0; s2 >>= 1) {
+    for (int s2 = NTF / 2; s2 > 0; s2 >>= 1) {
         if (t < s2) {
             const double a = red[t], b = red[t + s2];
             red[t] = (a < 0.0) ? b : ((b < 0.0) ? a : np_max(a, b));
@@ -550,7 +582,7 @@ __global__ void __launch_bounds__(NT) k_max_speed(mlamr_level lv, const double *
 constexpr int FIN_BLOCKS = 148;
 
 template <int M>
-__global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const double *__restrict__ src,
+__global__ void __launch_bounds__(NTF) k_step_finalize(mlamr_level lv, const double *__restrict__ src,
                                                       double *__restrict__ dst,
                                                       const int32_t *__restrict__ tiles,
                                                       int n_tiles, double dt,
@@ -558,7 +590,7 @@ __global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const doub
                                                       const double *tile_acc, double *acc,
                                                       int32_t *status, int32_t *bad_patch,
                                                       double *chunk, unsigned int *ticket) {
-    __shared__ double red[NT];
+    __shared__ double red[NTF];
     __shared__ int viol;
     __shared__ bool last;
     const int t = threadIdx.x;
@@ -568,8 +600,8 @@ __global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const doub
     const int t0 = blockIdx.x * per, t1 = min(n_tiles, t0 + per);
     for (int q = 0; q < K; ++q) {
         double v = 0.0;
-        for (int i = t0 + t; i < t1; i += NT) v = v + tile_acc[(int64_t)i * K + q];
-        const double sm = block_sum<NT>(v, red);
+        for (int i = t0 + t; i < t1; i += NTF) v = v + tile_acc[(int64_t)i * K + q];
+        const double sm = block_sum<NTF>(v, red);
         if (t == 0) chunk[blockIdx.x * K + q] = sm;
     }
     __threadfence();
@@ -589,7 +621,7 @@ __global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const doub
     const double dmin = lv.dx < lv.dy ? lv.dx : lv.dy;
     if (t == 0) viol = 0;
     __syncthreads();
-    for (int p = t; p < lv.num_patches; p += NT) {
+    for (int p = t; p < lv.num_patches; p += NTF) {
         const long long b = speed_bits[p];
         if (b < 0) continue;
         const double sp = __longlong_as_double(b);
@@ -609,7 +641,7 @@ __global__ void __launch_bounds__(NT) k_step_finalize(mlamr_level lv, const doub
         const double sp = __longlong_as_double(b);
         if (!((sp * dt) / dmin > 1.0)) continue;
         const PatchView pv = patch_view(lv, p);
-        for (int idx = t; idx < pv.nx * pv.ny; idx += NT) {
+        for (int idx = t; idx < pv.nx * pv.ny; idx += NTF) {
             const int r = idx / pv.nx, c = idx - r * pv.nx;
             const int64_t k = pv.off + (int64_t)(r + MLAMR_G) * pv.NX + (c + MLAMR_G);
             for (int q = 0; q < 3 * M; ++q) dst[q * FS + k] = src[q * FS + k];
@@ -694,9 +726,9 @@ extern "C" int mlamr_step_finalize(mlamr_level lv, const double *src_state, doub
     double *chunk = sc.chunk;
     unsigned int *ticket = sc.ticket;
     switch (prm.num_layers) {
-        case 1: k_step_finalize<1><<<FIN_BLOCKS, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
-        case 2: k_step_finalize<2><<<FIN_BLOCKS, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
-        case 3: k_step_finalize<3><<<FIN_BLOCKS, NT, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
+        case 1: k_step_finalize<1><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
+        case 2: k_step_finalize<2><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
+        case 3: k_step_finalize<3><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
         default: return -1;
     }
     return (int)cudaGetLastError();
@@ -708,9 +740,9 @@ extern "C" int mlamr_max_speed_tiles(mlamr_level lv, const double *state, const 
     cudaStream_t st = as_stream(stream);
     if (n_tiles <= 0) return 0;
     switch (prm.num_layers) {
-        case 1: k_max_speed<1><<<n_tiles, NT, 0, st>>>(lv, state, tiles, prm, speed_bits); break;
-        case 2: k_max_speed<2><<<n_tiles, NT, 0, st>>>(lv, state, tiles, prm, speed_bits); break;
-        case 3: k_max_speed<3><<<n_tiles, NT, 0, st>>>(lv, state, tiles, prm, speed_bits); break;
+        case 1: k_max_speed<1><<<n_tiles, NTF, 0, st>>>(lv, state, tiles, prm, speed_bits); break;
+        case 2: k_max_speed<2><<<n_tiles, NTF, 0, st>>>(lv, state, tiles, prm, speed_bits); break;
+        case 3: k_max_speed<3><<<n_tiles, NTF, 0, st>>>(lv, state, tiles, prm, speed_bits); break;
         default: return -1;
     }
     return (int)cudaGetLastError();
