@@ -55,8 +55,8 @@ struct StepSmem {
     double v[M][NPAD];                   // transverse velocity per layer
     double F[2 * M][NFLUX];              // (Fh, Fm) per layer at interface (r,c)-(r,c)+step
     double src[M > 1 ? M - 1 : 1][NPAD]; // coupling sources of layers 1..M-1
-    double red[NT];
-    long long redi[NT];
+    double red[(M + 2) * (NT / 32)];
+    long long redi[NT / 32];
     unsigned char cowet[NPAD];
     unsigned char wetcol[NPAD];
 };
@@ -74,6 +74,14 @@ struct StepSmem {
         if (c < (c0) || c >= (c1)) continue;                             \
         __VA_ARGS__                                                      \
     }
+
+// Per-launch constants, divided on the host (IEEE division, so the values
+// are the ones the device's `/` would give).
+struct StepConst {
+    double lam_x, lam_y;  // dt / dx, dt / dy
+    double rr[4][4];      // rho_k / rho_m for k < m
+    double coef;          // g * (1 - rho_0 / rho_1), the shear bound (physics.py:306)
+};
 
 // Reconstruction bottoms of layer m at a cell (physics.py:200-207, 105-110):
 // co-wet pairs use Zc (0 for upper layers, B for the bottom layer), others
@@ -228,6 +236,7 @@ __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             }
             s.F[2 * m][kl] = fh;
             s.F[2 * m + 1][kl] = fm;
+
         }
         // coupling sources of layers >= 1 for the interface's upper cell
         // (physics.py:208-211), on the pre-sweep state
@@ -326,7 +335,7 @@ template <int M, bool YFIRST>
 __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, const double *__restrict__ src,
                                              double *__restrict__ dst,
                                              const int32_t *__restrict__ tiles, double dt,
-                                             mlamr_params prm, long long *speed_bits,
+                                             mlamr_params prm, StepConst kc, long long *speed_bits,
                                              double *tile_acc, const int32_t *status) {
     if (status != nullptr && *status != 0) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -373,14 +382,8 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);
-    // density ratios rho_k / rho_m, only the k < m entries the sources use
-    double rr[4][4];
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
-
-    const double lam_x = dt / lv.dx, lam_y = dt / lv.dy;
+    const double(&rr)[4][4] = kc.rr;
+    const double lam_x = kc.lam_x, lam_y = kc.lam_y;
     const double y_x = recip_nr(lv.dx), y_y = recip_nr(lv.dy);
     asm volatile("cp.async.wait_group 0;\n" ::);
     __syncthreads();
@@ -402,7 +405,7 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
 #pragma unroll
     for (int m = 0; m < M; ++m) negs[m] = 0.0;
     long long fixes = 0, repairs = 0;
-    const double coef = prm.gravity * (1.0 - rr[0][1]);
+    const double coef = kc.coef;
     FOR_RECT(1, ny2 - 1, 1, nx2 - 1, {
         const int k = r * PX + c;
         double h[M], hu[M], hv[M];
@@ -667,10 +670,17 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
         configured[y_first ? 1 : 0] = true;
     }
     if (n_tiles <= 0) return 0;
+    StepConst kc;
+    kc.lam_x = dt / lv.dx;
+    kc.lam_y = dt / lv.dy;
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b)
+            kc.rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
+    kc.coef = (M > 1) ? prm.gravity * (1.0 - kc.rr[0][1]) : 0.0;
     if (y_first)
-        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, speed_bits, tile_acc, status);
+        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status);
     else
-        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, speed_bits, tile_acc, status);
+        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status);
     return (int)cudaGetLastError();
 }
 

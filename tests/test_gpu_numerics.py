@@ -40,3 +40,14 @@ def test_div_fast_special_values():
     a, b = np.meshgrid(vals, vals)
     bad, slow = _run(a.ravel().copy(), b.ravel().copy())
     assert bad == 0
+
+
+def test_div_fast_zero_dividend():
+    # +-0 over normal finite divisors of every magnitude: signed zero, exact
+    rng = np.random.default_rng(12)
+    n = 1 << 20
+    b = rng.standard_normal(n) * np.exp(rng.uniform(-700, 700, n))
+    b = b[np.isfinite(b) & (np.abs(b) >= 2.2250738585072014e-308)]
+    a = np.where(rng.random(len(b)) < 0.5, 0.0, -0.0)
+    bad, slow = _run(a, b.copy())
+    assert bad == 0
