@@ -205,6 +205,16 @@ int mlamr_copy_segments(const double *src, int64_t src_stride, double *dst, int6
                         const int64_t *segments, int n_segments, int max_len, int nplanes,
                         void *stream);
 
+/* Frame records of one level (frames.frame_from_hierarchy + write_frame,
+ * frames.py:72-100, 141-163): for each patch p (or each entry of
+ * patch_list), writes at out + rec_off[p] (8-byte units) the five int64
+ * (level_index, lo_i, lo_j, hi_i, hi_j) and the interior planes bathymetry,
+ * h_0, hu_0, hv_0, h_1, ... (row-major, x fastest) -- the reference's binary
+ * patch record, so the host writes header + one contiguous body. */
+int mlamr_pack_frame(mlamr_level lv, const double *state, int level_index, const int64_t *rec_off,
+                     const int32_t *patch_list, int n_list, int blocks_per_patch, double *out,
+                     void *stream);
+
 /* Full reference flag rule on the device (regrid.flag_cells +
  * nesting_allowed, regrid.py:58-101, 185-211): from mlamr_flag_cells' bits,
  * flags = dilate(amplitude | wet_m & dilate(dry_m)) & covered & allowed and

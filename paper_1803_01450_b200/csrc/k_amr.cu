@@ -919,6 +919,48 @@ extern "C" int mlamr_selftest_div(const double *a, const double *b, int n, unsig
     return (int)cudaGetLastError();
 }
 
+// Frame records from a device pool (frames.write_frame / frame_from_hierarchy,
+// frames.py:72-100, 141-163 of the reference): record p starts at element
+// rec_off[p] of `out` (8-byte units) with five little-endian int64 (level,
+// lo_i, lo_j, hi_i, hi_j), then the interior of bathymetry, h_0, hu_0, hv_0,
+// h_1, ... as row-major ny x nx float64 planes.  Grid: (x blocks, patches);
+// patch_list (optional) selects the patches, e.g. a rank's owned ones.
+__global__ void k_pack_frame(mlamr_level lv, const double *__restrict__ state, int level_index,
+                             const int64_t *__restrict__ rec_off, const int32_t *__restrict__ patch_list,
+                             double *__restrict__ out) {
+    const int p = patch_list ? patch_list[blockIdx.y] : blockIdx.y;
+    const PatchView pv = patch_view(lv, p);
+    const int M = lv.num_layers;
+    const int64_t n = (int64_t)pv.nx * pv.ny;
+    double *rec = out + rec_off[p];
+    if (blockIdx.x == 0 && threadIdx.x < 5) {
+        const int64_t hdr[5] = {level_index, pv.lo_i, pv.lo_j, pv.lo_i + pv.nx - 1, pv.lo_j + pv.ny - 1};
+        reinterpret_cast<int64_t *>(rec)[threadIdx.x] = hdr[threadIdx.x];
+    }
+    double *body = rec + 5;
+    const int64_t FS = lv.field_stride;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(i / pv.nx), c = (int)(i - (int64_t)r * pv.nx);
+        const int64_t k = pv.off + (int64_t)(r + MLAMR_G) * pv.NX + (c + MLAMR_G);
+        body[i] = lv.bathy[k];
+        for (int m = 0; m < M; ++m) {
+            body[(1 + 3 * m) * n + i] = state[m * FS + k];
+            body[(2 + 3 * m) * n + i] = state[(M + m) * FS + k];
+            body[(3 + 3 * m) * n + i] = state[(2 * M + m) * FS + k];
+        }
+    }
+}
+
+extern "C" int mlamr_pack_frame(mlamr_level lv, const double *state, int level_index, const int64_t *rec_off,
+                                const int32_t *patch_list, int n_list, int blocks_per_patch, double *out,
+                                void *stream) {
+    const int np = patch_list ? n_list : lv.num_patches;
+    if (np <= 0) return 0;
+    dim3 grid(blocks_per_patch > 0 ? blocks_per_patch : 1, np);
+    k_pack_frame<<<grid, NTA, 0, as_stream(stream)>>>(lv, state, level_index, rec_off, patch_list, out);
+    return (int)cudaGetLastError();
+}
+
 // Full reference flag rule + nesting mask on the device.  `bits` from
 // mlamr_flag_cells; scratch = 3 byte maps of ny*nx.  Outputs: flags
 // (0/1, already & covered & allowed) and allowed = erode(covered, 1).

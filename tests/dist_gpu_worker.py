@@ -71,6 +71,15 @@ def main():
         ref.advance_coarse_step(dt)
         sh.advance_coarse_step(dt)
         compare(f"step{k}")
+    # frames: rank 0 assembles every rank's owned records into the bytes
+    # the single-GPU driver writes
+    from paper_1803_01450_b200 import frames as F
+    fb = F.frame_bytes(sh)
+    fa = F.frame_bytes(ref)
+    if rank == 0:
+        assert fb == fa, ("frame", len(fa), len(fb or b""))
+    else:
+        assert fb is None
     a, b = ref.finish(), sh.finish()
     assert a.total_cell_updates == b.total_cell_updates, (a.total_cell_updates, b.total_cell_updates)
     assert a.num_regrids == b.num_regrids

@@ -307,6 +307,40 @@ def make_run_cases():
     _save("run_shelf_small.npz", **recs)
 
 
+def make_frame_cases():
+    """Frames the reference itself writes (frames.frame_from_hierarchy +
+    write_frame) for configs/shelf_demo_small.cfg at t=0 and after two
+    coarse steps, binary and text; the t=0 text frame must equal the
+    reference's committed fixture tests/fixtures/frames/shelf_small_frame0000.txt."""
+    import io
+    import tempfile
+    from mlamr import frames as F
+    cfg = parse_config("/root/reference/pkg/configs/shelf_demo_small.cfg")
+    sim = Simulation(cfg, workers=1)
+    recs = {}
+
+    def grab(tag):
+        fr = F.frame_from_hierarchy(sim.hier, sim.time, cfg.eta_rest)
+        for text in (False, True):
+            with tempfile.NamedTemporaryFile(suffix=".frame") as tf:
+                F.write_frame(fr, tf.name, text_mode=text)
+                recs[f"{tag}_{'txt' if text else 'bin'}"] = np.frombuffer(open(tf.name, "rb").read(), np.uint8)
+
+    grab("t0")
+    fixture = "/root/reference/pkg/tests/fixtures/frames/shelf_small_frame0000.txt"
+    assert recs["t0_txt"].tobytes() == open(fixture, "rb").read(), "t0 text frame differs from the fixture"
+    dts = []
+    for _ in range(2):
+        dt = cfg.dt_max
+        for p in sim.hier.patches[1]:
+            dt = min(dt, physics.stable_dt(p, sim.params, cfg.cfl, cfg.dt_max))
+        dts.append(dt)
+        sim.advance_coarse_step(dt)
+    grab("s2")
+    recs["dts"] = np.array(dts)
+    _save("frames_shelf_small.npz", **recs)
+
+
 def main():
     rng = np.random.default_rng(20180305)
     make_step_cases(rng)
@@ -314,6 +348,7 @@ def main():
     make_blockmean_cases(rng)
     make_cluster_cases(rng)
     make_run_cases()
+    make_frame_cases()
 
 
 if __name__ == "__main__":
