@@ -29,7 +29,7 @@ import ctypes
 import time
 from collections import defaultdict
 from contextlib import contextmanager
-from dataclasses import dataclass, field, replace
+from dataclasses import asdict, dataclass, field, replace
 
 import numpy as np
 import torch
@@ -47,19 +47,33 @@ _LOG_STEP_BYTES = bool(__import__("os").environ.get("MLAMR_LOG_STEP_BYTES"))
 
 @dataclass
 class RunStats:
-    """Counters of one run (driver.py:44-86)."""
+    """Counters and timers of one run (driver.py:44-78): same fields and
+    the same ``to_json`` layout as the reference's stats.json."""
+    wall_time: float = 0.0
+    cpu_time: float = 0.0
     total_cell_updates: int = 0
     cell_updates_per_level: dict = field(default_factory=dict)
     num_coarse_steps: int = 0
     num_regrids: int = 0
-    hyperbolicity_warnings: int = 0
-    wet_prefix_repairs: int = 0
-    clipped_mass: list = field(default_factory=list)
+    workers: int = 1
+    amr_enabled: bool = True
+    initial_mass: list = field(default_factory=list)
+    final_mass: list = field(default_factory=list)
+    mass_drift: list = field(default_factory=list)
     refine_delta: list = field(default_factory=list)
     derefine_delta: list = field(default_factory=list)
     sync_delta: list = field(default_factory=list)
-    initial_mass: list = field(default_factory=list)
-    final_mass: list = field(default_factory=list)
+    hyperbolicity_warnings: int = 0
+    wet_prefix_repairs: int = 0
+    clipped_mass: list = field(default_factory=list)
+
+    def to_json(self, path) -> None:
+        import json
+        data = asdict(self)
+        data["cell_updates_per_level"] = {str(k): int(v) for k, v in self.cell_updates_per_level.items()}
+        with open(path, "w") as f:
+            json.dump(data, f, indent=2, sort_keys=True, default=lambda o: o.item() if hasattr(o, "item") else str(o))
+            f.write("\n")
 
 
 class Simulation:
@@ -546,6 +560,39 @@ class Simulation:
             self.advance_coarse_step(dt)
         return self.finish()
 
+    def run_until(self, t_final: float, frame_times=(), frame_callback=None) -> RunStats:
+        """The reference's time loop (driver.py:312-362): level-1 stable dt,
+        clipped to land exactly on the next frame time or t_final, with
+        ``frame_callback(sim, time, index)`` at every due frame time.  Wall
+        and CPU timers cover the integration loop only."""
+        eps = 1e-12 * max(1.0, t_final)
+        times = list(frame_times)
+        idx = 0
+
+        def emit():
+            nonlocal idx
+            while idx < len(times) and times[idx] <= self.time + eps:
+                if frame_callback is not None:
+                    frame_callback(self, self.time, idx)
+                idx += 1
+
+        emit()
+        while self.time < t_final - eps:
+            wall0, cpu0 = time.perf_counter(), time.process_time()
+            dt = self.choose_dt()
+            target = t_final if idx >= len(times) else min(t_final, times[idx])
+            clipped = self.time + dt >= target - eps
+            if clipped:
+                dt = target - self.time
+            self.apply_dynamic_rt(dt)
+            self.advance_coarse_step(dt)
+            if clipped:
+                self.time = target
+            self.stats.wall_time += time.perf_counter() - wall0
+            self.stats.cpu_time += time.process_time() - cpu0
+            emit()
+        return self.finish()
+
     def finish(self) -> RunStats:
         self.stream.synchronize()
         acc = self.acc.cpu().numpy()
@@ -557,6 +604,8 @@ class Simulation:
         self.stats.refine_delta = list(d[0])
         self.stats.derefine_delta = list(d[1])
         self.stats.final_mass = list(self._mass_prev)
+        if self.stats.initial_mass:
+            self.stats.mass_drift = [f - i for f, i in zip(self.stats.final_mass, self.stats.initial_mass)]
         return self.stats
 
     # -- checkpoint: host snapshot / restore (pinned host buffers) ----------------------------
@@ -628,3 +677,41 @@ class Simulation:
             h, hu, hv, b = pool.patch_arrays(p, host=host)
             out.append((tuple(int(v) for v in pool.boxes[p]), h, hu, hv, b))
         return out
+
+
+def run_simulation(problem, out_dir=None, t_final: float | None = None, frame_times=(), text_frames: bool = False,
+                   n_coarse: int | None = None, sim_cls=None, **kw) -> RunStats:
+    """``run_simulation`` of the reference (driver.py:365-410): run, write
+    ``frameNNNN.bin|txt`` at the frame times and ``stats.json`` into
+    ``out_dir``; on a numerical abort or CFL violation write ``abort.*``
+    and the partial stats before re-raising.  Frames come straight from the
+    device pools (frames.py).  ``n_coarse`` runs a fixed number of coarse
+    steps instead of a time span (frames at t=0 and at the end)."""
+    from pathlib import Path
+    from . import frames as F
+    sim = (sim_cls or Simulation)(problem, **kw)
+    out = Path(out_dir) if out_dir is not None else None
+    if out is not None and getattr(sim, "rank", 0) == 0:
+        out.mkdir(parents=True, exist_ok=True)
+    ext = "txt" if text_frames else "bin"
+
+    def frame_cb(s, t, index):
+        if out is not None:
+            F.write_frame(s, out / f"frame{index:04d}.{ext}", text_frames)
+
+    try:
+        if n_coarse is not None:
+            frame_cb(sim, sim.time, 0)
+            stats = sim.run(n_coarse)
+            frame_cb(sim, sim.time, 1)
+        else:
+            stats = sim.run_until(t_final, frame_times, frame_cb)
+    except (NumericalAbortError, CflViolationError):
+        if out is not None:
+            F.write_frame(sim, out / f"abort.{ext}", text_frames)
+            if getattr(sim, "rank", 0) == 0:
+                sim.stats.to_json(out / "stats.json")
+        raise
+    if out is not None and getattr(sim, "rank", 0) == 0:
+        stats.to_json(out / "stats.json")
+    return stats

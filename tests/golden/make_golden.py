@@ -338,6 +338,20 @@ def make_frame_cases():
         sim.advance_coarse_step(dt)
     grab("s2")
     recs["dts"] = np.array(dts)
+    # the full run_simulation (driver.py:365-410) to t_final with its frame
+    # times: frame files and stats.json
+    import json
+    from mlamr.driver import run_simulation
+    with tempfile.TemporaryDirectory() as d:
+        run_simulation(cfg, out_dir=d, workers=1)
+        for k in range(len(cfg.frame_times)):
+            recs[f"run_frame{k}"] = np.frombuffer(open(os.path.join(d, f"frame{k:04d}.bin"), "rb").read(), np.uint8)
+        st = json.load(open(os.path.join(d, "stats.json")))
+    for key in ("wall_time", "cpu_time"):
+        st.pop(key)
+    recs["run_stats_json"] = np.frombuffer(json.dumps(st, sort_keys=True).encode(), np.uint8)
+    recs["run_t_final"] = np.asarray(cfg.t_final)
+    recs["run_frame_times"] = np.asarray(cfg.frame_times)
     _save("frames_shelf_small.npz", **recs)
 
 

@@ -50,3 +50,27 @@ def test_write_frame_and_compare(tmp_path):
     a, b = F.read_frame(tmp_path / "a.bin"), F.read_frame(tmp_path / "b.bin")
     assert a.time == 0.0 and b.time > 0.0
     assert F.l1_diff(a, b)["eta_1_linf"] > 0.0
+
+
+def test_run_simulation_frames_and_stats_match_reference(tmp_path):
+    """run_simulation to t_final with the config's frame times (dt clipped
+    onto every frame time): frame files identical to the reference's, and
+    the same stats.json counters."""
+    import json
+    from shelf_problem import shelf_problem
+    from paper_1803_01450_b200.driver import run_simulation
+    z = load_golden("frames_shelf_small.npz")
+    st = run_simulation(shelf_problem(), out_dir=tmp_path, t_final=float(z["run_t_final"]),
+                        frame_times=[float(t) for t in z["run_frame_times"]])
+    for k in range(len(z["run_frame_times"])):
+        mine = (tmp_path / f"frame{k:04d}.bin").read_bytes()
+        assert mine == z[f"run_frame{k}"].tobytes(), k
+    ref = json.loads(z["run_stats_json"].tobytes())
+    got = json.loads((tmp_path / "stats.json").read_text())
+    for key in ("total_cell_updates", "num_coarse_steps", "num_regrids", "hyperbolicity_warnings",
+                "wet_prefix_repairs", "cell_updates_per_level", "amr_enabled", "workers"):
+        assert got[key] == ref[key], key
+    for key in ("initial_mass", "final_mass", "mass_drift", "refine_delta", "derefine_delta", "sync_delta",
+                "clipped_mass"):
+        np.testing.assert_allclose(got[key], ref[key], rtol=1e-9, atol=1e-12, err_msg=key)
+    assert st.wall_time > 0.0
