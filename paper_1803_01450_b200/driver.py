@@ -297,6 +297,9 @@ class Simulation:
         else:
             raise ValueError(rule)
         allowed = nesting_allowed(pool.boxes, s.ny, s.nx)
+        region = self.pb.region_mask(level)
+        if region is not None:
+            allowed = allowed & region
         return f & allowed, allowed
 
     def flags_for(self, level: int) -> np.ndarray:
@@ -318,7 +321,20 @@ class Simulation:
             self._call(self.lib.mlamr_flags_reference, b["bits"].data_ptr(), s.ny, s.nx, self.M,
                        self.pb.buffer_width, b["flags"].data_ptr(), b["allowed"].data_ptr(),
                        b["scratch"].data_ptr(), self.sh)
+            region = self._region_mask_d(level)
+            if region is not None:   # configured allowed rectangles (regrid.py:197-209)
+                b["flags"].mul_(region)
+                b["allowed"].mul_(region)
         return b["flags"], b["allowed"]
+
+    def _region_mask_d(self, level: int):
+        if not self.pb.allowed_regions:
+            return None
+        key = ("region", level)
+        if key not in self._flagbuf:
+            m = self.pb.region_mask(level).astype(np.uint8).reshape(-1)
+            self._flagbuf[key] = arena().upload(m, self.dev, self.stream)
+        return self._flagbuf[key]
 
     def _reduce_flag_bits(self, bits) -> None:
         """Single GPU: nothing to combine (the sharded driver all-reduces)."""

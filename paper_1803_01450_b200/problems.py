@@ -107,7 +107,26 @@ class Problem:
     # how levels >= 2 get data at t=0: "scenario" (the initial condition,
     # regrid.py:284-286) or "refine" (interpolated from the level below)
     init_mode: str = "scenario"
+    # physical rectangles (x0, x1, y0, y1) refinement is confined to, by a
+    # cell-centre test (regrid.nesting_allowed, regrid.py:185-211)
+    allowed_regions: tuple = ()
+    # run length and frame times of a run file (config.py); 0 / () = unset
+    t_final: float = 0.0
+    frame_times: tuple = ()
     notes: str = ""
+
+    def region_mask(self, level: int) -> Optional[np.ndarray]:
+        """Cells of ``level`` whose centre lies in an allowed region (None
+        when no regions are configured)."""
+        if not self.allowed_regions:
+            return None
+        lev, nx, ny, dx, dy = self.level_specs()[level - 1][:5]
+        xc = self.domain[0] + (np.arange(nx) + 0.5) * dx
+        yc = self.domain[2] + (np.arange(ny) + 0.5) * dy
+        inside = np.zeros((ny, nx), bool)
+        for x0, x1, y0, y1 in self.allowed_regions:
+            inside |= (xc[None, :] >= x0) & (xc[None, :] <= x1) & (yc[:, None] >= y0) & (yc[:, None] <= y1)
+        return inside
 
     # -- geometry (mesh.py:325-375) -----------------------------------------
     def level_specs(self):

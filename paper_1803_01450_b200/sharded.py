@@ -205,6 +205,9 @@ class ShardedSimulation(Simulation):
             f = self.pb.bernoulli_flags(level, self.steps[level])
             f = dilate(f, self.pb.flag_rule[2]) & covered
             allowed = nesting_allowed(self.layout[level], s.ny, s.nx)
+            region = self.pb.region_mask(level)
+            if region is not None:
+                allowed = allowed & region
             return f & allowed, allowed
         return super().flags_and_allowed(level)
 

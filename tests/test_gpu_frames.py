@@ -74,3 +74,32 @@ def test_run_simulation_frames_and_stats_match_reference(tmp_path):
                 "clipped_mass"):
         np.testing.assert_allclose(got[key], ref[key], rtol=1e-9, atol=1e-12, err_msg=key)
     assert st.wall_time > 0.0
+
+
+def test_run_file_to_reference_frames(tmp_path):
+    """A run file through config.problem_from_config (the reference's
+    Scenario, no captured arrays) reproduces the reference's run frames."""
+    import os
+    from paper_1803_01450_b200.config import problem_from_config
+    from paper_1803_01450_b200.driver import run_simulation
+    z = load_golden("frames_shelf_small.npz")
+    pb = problem_from_config(os.path.join(os.path.dirname(__file__), "configs", "shelf_small.cfg"))
+    run_simulation(pb, out_dir=tmp_path, t_final=pb.t_final, frame_times=pb.frame_times)
+    for k in range(len(pb.frame_times)):
+        assert (tmp_path / f"frame{k:04d}.bin").read_bytes() == z[f"run_frame{k}"].tobytes(), k
+
+
+def test_cli_run_and_compare(tmp_path):
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cfg = os.path.join(root, "tests", "configs", "shelf_small.cfg")
+    r = subprocess.run([sys.executable, "-m", "paper_1803_01450_b200", "run", cfg, "--out", str(tmp_path)],
+                       capture_output=True, text=True, cwd=root, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert (tmp_path / "stats.json").exists() and (tmp_path / "frame0002.bin").exists()
+    r = subprocess.run([sys.executable, "-m", "paper_1803_01450_b200", "compare", str(tmp_path / "frame0000.bin"),
+                        str(tmp_path / "frame0002.bin"), "--norm", "all"], capture_output=True, text=True,
+                       cwd=root, timeout=300)
+    assert r.returncode == 0 and "eta_1_l1" in r.stdout and "h_2_linf" in r.stdout, r.stdout + r.stderr
