@@ -289,15 +289,22 @@ class Scenario:
         return h, hu, hv
 
 
-def problem_from_config(cfg) -> Problem:
+def problem_from_config(cfg, uniform_fine: bool = False) -> Problem:
     """A Problem for the GPU driver from a RunConfig (or a path to a run
     file): geometry, layer parameters, regrid policy and allowed regions,
-    frame times, and the scenario's per-level bed means and initial state."""
+    frame times, and the scenario's per-level bed means and initial state.
+    ``uniform_fine`` is the reference's ``--no-amr`` run (driver.py:104-107,
+    config.py:191-206): one level at the finest level's resolution."""
     if not isinstance(cfg, RunConfig):
         cfg = parse_config(cfg)
     rx, ry = list(cfg.refine_x), list(cfg.refine_y)
+    nx0, ny0 = cfg.nx, cfg.ny
+    if uniform_fine and rx:
+        for a, b in zip(rx, ry):
+            nx0, ny0 = nx0 * a, ny0 * b
+        rx, ry = [], []
     pb = Problem(
-        name=cfg.name, domain=cfg.domain, coarse_nx=cfg.nx, coarse_ny=cfg.ny, ratios_x=rx, ratios_y=ry,
+        name=cfg.name, domain=cfg.domain, coarse_nx=nx0, coarse_ny=ny0, ratios_x=rx, ratios_y=ry,
         ratios_t=[max(a, b) for a, b in zip(rx, ry)], num_layers=cfg.num_layers, densities=cfg.densities,
         gravity=cfg.gravity, dry_tolerance=cfg.dry_tolerance, eta_rest=cfg.eta_rest,
         boundaries=cfg.boundaries, cfl=cfg.cfl, dt_max=cfg.dt_max, wave_tolerance=tuple(cfg.wave_tolerance),
@@ -317,4 +324,5 @@ def problem_from_config(cfg) -> Problem:
     M, tol = cfg.num_layers, cfg.dry_tolerance
     pb.ic = lambda p, level, xc, yc, jj, ii, B: sc.initial_state(xc, B, M, tol)
     pb.scenario = sc
+    pb.amr_enabled = bool(rx)
     return pb

@@ -706,6 +706,7 @@ def run_simulation(problem, out_dir=None, t_final: float | None = None, frame_ti
     from pathlib import Path
     from . import frames as F
     sim = (sim_cls or Simulation)(problem, **kw)
+    sim.stats.amr_enabled = bool(getattr(problem, "amr_enabled", len(problem.ratios_x) > 0))
     out = Path(out_dir) if out_dir is not None else None
     if out is not None and getattr(sim, "rank", 0) == 0:
         out.mkdir(parents=True, exist_ok=True)

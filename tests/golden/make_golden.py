@@ -350,6 +350,15 @@ def make_frame_cases():
     for key in ("wall_time", "cpu_time"):
         st.pop(key)
     recs["run_stats_json"] = np.frombuffer(json.dumps(st, sort_keys=True).encode(), np.uint8)
+    # the uniform-grid run (--no-amr, driver.py:104-107) at the finest resolution
+    with tempfile.TemporaryDirectory() as d:
+        run_simulation(cfg, out_dir=d, workers=1, amr=False)
+        recs["uniform_frame_last"] = np.frombuffer(
+            open(os.path.join(d, f"frame{len(cfg.frame_times) - 1:04d}.bin"), "rb").read(), np.uint8)
+        st = json.load(open(os.path.join(d, "stats.json")))
+    for key in ("wall_time", "cpu_time"):
+        st.pop(key)
+    recs["uniform_stats_json"] = np.frombuffer(json.dumps(st, sort_keys=True).encode(), np.uint8)
     recs["run_t_final"] = np.asarray(cfg.t_final)
     recs["run_frame_times"] = np.asarray(cfg.frame_times)
     _save("frames_shelf_small.npz", **recs)

@@ -103,3 +103,22 @@ def test_cli_run_and_compare(tmp_path):
                         str(tmp_path / "frame0002.bin"), "--norm", "all"], capture_output=True, text=True,
                        cwd=root, timeout=300)
     assert r.returncode == 0 and "eta_1_l1" in r.stdout and "h_2_linf" in r.stdout, r.stdout + r.stderr
+
+
+def test_uniform_run_matches_reference_no_amr(tmp_path):
+    """The reference's --no-amr run (one level at the finest resolution)."""
+    import json
+    import os
+    from paper_1803_01450_b200.config import problem_from_config
+    from paper_1803_01450_b200.driver import run_simulation
+    z = load_golden("frames_shelf_small.npz")
+    pb = problem_from_config(os.path.join(os.path.dirname(__file__), "configs", "shelf_small.cfg"),
+                             uniform_fine=True)
+    assert pb.num_levels == 1 and (pb.coarse_nx, pb.coarse_ny) == (256, 64)
+    run_simulation(pb, out_dir=tmp_path, t_final=pb.t_final, frame_times=pb.frame_times)
+    last = len(pb.frame_times) - 1
+    assert (tmp_path / f"frame{last:04d}.bin").read_bytes() == z["uniform_frame_last"].tobytes()
+    ref = json.loads(z["uniform_stats_json"].tobytes())
+    got = json.loads((tmp_path / "stats.json").read_text())
+    for key in ("total_cell_updates", "num_coarse_steps", "num_regrids", "amr_enabled", "cell_updates_per_level"):
+        assert got[key] == ref[key], key
