@@ -205,6 +205,14 @@ int mlamr_copy_segments(const double *src, int64_t src_stride, double *dst, int6
                         const int64_t *segments, int n_segments, int max_len, int nplanes,
                         void *stream);
 
+/* Summed-area table for the clustering bisection (regrid.cluster_flags,
+ * regrid.py:129-182): sat is int32 [(ny+1)*(nx+1)] with
+ * sat[(j+1)*(nx+1)+(i+1)] = sum over [0,j]x[0,i] of map (invert=0) or
+ * 1-map (invert=1), zero first row/column; scratch is int32
+ * [ceil(ny/32)*nx].  Exact integer sums. */
+int mlamr_sat_u8(const uint8_t *map, int ny, int nx, int invert, int32_t *sat, int32_t *scratch,
+                 void *stream);
+
 /* Frame records of one level (frames.frame_from_hierarchy + write_frame,
  * frames.py:72-100, 141-163): for each patch p (or each entry of
  * patch_list), writes at out + rec_off[p] (8-byte units) the five int64

@@ -919,6 +919,87 @@ extern "C" int mlamr_selftest_div(const double *a, const double *b, int n, unsig
     return (int)cudaGetLastError();
 }
 
+// Summed-area table of a 0/1 byte map for the clustering bisection
+// (regrid.cluster_flags, regrid.py:129-182, evaluated from box sums):
+// sat[(j+1)*(nx+1) + (i+1)] = sum of v over [0,j] x [0,i], v = map or
+// 1 - map (invert), row 0 and column 0 zero.  Integer sums, so the result
+// is exact in any order: one warp scans each row with shuffles, then the
+// columns are scanned in row segments (segment sums, their scan, the add).
+constexpr int SAT_SEG = 32;  // rows per column segment
+
+__global__ void k_sat_rows(const uint8_t *__restrict__ map, int ny, int nx, int invert, int32_t *__restrict__ sat) {
+    const int lane = threadIdx.x & 31;
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (row > ny) return;
+    int32_t *out = sat + (int64_t)row * (nx + 1);
+    if (row == 0) {
+        for (int i = lane; i <= nx; i += 32) out[i] = 0;
+        return;
+    }
+    const uint8_t *in = map + (int64_t)(row - 1) * nx;
+    if (lane == 0) out[0] = 0;
+    int carry = 0;
+    for (int i0 = 0; i0 < nx; i0 += 32) {
+        const int i = i0 + lane;
+        int v = (i < nx) ? (invert ? 1 - (int)in[i] : (int)in[i]) : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (i < nx) out[i + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+}
+
+__global__ void k_sat_cols_local(int32_t *__restrict__ sat, int ny, int nx, int32_t *__restrict__ segsum) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;  // column 1..nx
+    const int seg = blockIdx.y;
+    if (i > nx) return;
+    const int j0 = 1 + seg * SAT_SEG, j1 = min(ny, j0 + SAT_SEG - 1);
+    int acc = 0;
+    for (int j = j0; j <= j1; ++j) {
+        int32_t *q = sat + (int64_t)j * (nx + 1) + i;
+        acc += *q;
+        *q = acc;
+    }
+    segsum[(int64_t)seg * nx + (i - 1)] = acc;
+}
+
+__global__ void k_sat_cols_scan(int32_t *__restrict__ segsum, int nseg, int nx) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nx) return;
+    int acc = 0;
+    for (int s = 0; s < nseg; ++s) {  // exclusive scan over segments
+        const int v = segsum[(int64_t)s * nx + i];
+        segsum[(int64_t)s * nx + i] = acc;
+        acc += v;
+    }
+}
+
+__global__ void k_sat_cols_add(int32_t *__restrict__ sat, int ny, int nx, const int32_t *__restrict__ segsum) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x + 1;
+    const int seg = blockIdx.y + 1;  // segment 0 has offset 0
+    if (i > nx) return;
+    const int off = segsum[(int64_t)seg * nx + (i - 1)];
+    const int j0 = 1 + seg * SAT_SEG, j1 = min(ny, j0 + SAT_SEG - 1);
+    for (int j = j0; j <= j1; ++j) sat[(int64_t)j * (nx + 1) + i] += off;
+}
+
+extern "C" int mlamr_sat_u8(const uint8_t *map, int ny, int nx, int invert, int32_t *sat, int32_t *scratch,
+                            void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (ny <= 0 || nx <= 0) return 0;
+    const int wpb = 8;
+    k_sat_rows<<<(ny + 1 + wpb - 1) / wpb, 32 * wpb, 0, st>>>(map, ny, nx, invert, sat);
+    const int nseg = (ny + SAT_SEG - 1) / SAT_SEG;
+    const int cb = (nx + 127) / 128;
+    k_sat_cols_local<<<dim3(cb, nseg), 128, 0, st>>>(sat, ny, nx, scratch);
+    k_sat_cols_scan<<<cb, 128, 0, st>>>(scratch, nseg, nx);
+    if (nseg > 1) k_sat_cols_add<<<dim3(cb, nseg - 1), 128, 0, st>>>(sat, ny, nx, scratch);
+    return (int)cudaGetLastError();
+}
+
 // Frame records from a device pool (frames.write_frame / frame_from_hierarchy,
 // frames.py:72-100, 141-163 of the reference): record p starts at element
 // rec_off[p] of `out` (8-byte units) with five little-endian int64 (level,

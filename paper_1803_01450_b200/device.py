@@ -82,9 +82,13 @@ _ARENA = None
 # stream-ordered (everything runs on the driver's stream).
 _RECYCLE: list = []
 ALLOC_STATS = {"fresh": 0, "fresh_bytes": 0, "reused": 0}
+POOL_PROF = __import__("collections").defaultdict(float)   # host seconds inside LevelPool()
 
 
 def acquire(numel: int, dtype, device, stream) -> torch.Tensor:
+    device = torch.device(device)
+    if device.type == "cuda" and device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
     best = None
     for k, t in enumerate(_RECYCLE):
         if t.dtype == dtype and t.device == device and t.numel() >= numel:
@@ -108,6 +112,26 @@ def release(t: torch.Tensor) -> None:
     # bound the cache: keep the 16 largest buffers
     _RECYCLE.sort(key=lambda x: -x.numel())
     del _RECYCLE[16:]
+
+
+def reserve(nbytes: int, device, stream) -> None:
+    """Warm the caching allocator with ``nbytes`` of device memory.
+
+    Regrids replace level pools with ones of similar size; whenever a pool
+    outgrows the recycled buffers its buffers come from cudaMalloc, which
+    on a fresh GPU costs tens of milliseconds per GB (first-touch page
+    mapping) inside the time loop.  One large allocation released into
+    PyTorch's cache up front turns those into cache hits (cached blocks are
+    split on demand)."""
+    if nbytes <= 0:
+        return
+    free, _total = torch.cuda.mem_get_info(device)
+    n = int(min(nbytes, 0.8 * free))
+    if n <= 0:
+        return
+    with torch.cuda.stream(stream):
+        t = torch.empty(n, dtype=torch.uint8, device=device)
+    del t
 
 
 def arena() -> PinnedArena:
@@ -166,16 +190,26 @@ class LevelPool:
         self.FS = max(int(aligned.sum()), ALIGN)
         self.max_cells = int(size.max()) if self.P else 0
         self.max_interior = int((nx * ny).max()) if self.P else 0
+        import time as _t
+        _p = POOL_PROF
+        _t0 = _t.perf_counter()
         with torch.cuda.stream(stream):
             self.buf = [acquire(3 * M * self.FS, torch.float64, device, stream),
                         acquire(3 * M * self.FS, torch.float64, device, stream)]
             self.bathy = acquire(self.FS, torch.float64, device, stream)
+            _t1 = _t.perf_counter()
+            _p["acquire"] += _t1 - _t0
             for t in (self.buf[0], self.buf[1], self.bathy):
                 t.zero_()
+            _t2 = _t.perf_counter()
+            _p["zero"] += _t2 - _t1
             A = arena()
             self.box_d = A.upload(b.astype(np.int32), device, stream)
             self.off_d = A.upload(self.offsets, device, stream)
+            _t3 = _t.perf_counter()
+            _p["upload"] += _t3 - _t2
             tl = tile_list(b)
+            _p["tile_list"] += _t.perf_counter() - _t3
             if self.owned is not None and len(tl):
                 tl = tl[self.owned[tl[:, 0]]]
             self.tiles = tl
@@ -191,8 +225,10 @@ class LevelPool:
                     torch.zeros(1, dtype=torch.int32, device=device)
             self.speed_bits = torch.full((max(self.P, 1),), -1, dtype=torch.int64, device=device)
             mapn = (spec.nx + 2 * GHOST_WIDTH) * (spec.ny + 2 * GHOST_WIDTH)
+            _t4 = _t.perf_counter()
             self.own = acquire(mapn, torch.int32, device, stream).fill_(-1)
             self.gown = acquire(mapn, torch.int32, device, stream).fill_(-1) if need_gown else None
+            _p["maps"] += _t.perf_counter() - _t4
         self.child: Optional[torch.Tensor] = None   # finer level's coarsened owner map
         self.cur = 0
         self.ghosts_in_cur = False

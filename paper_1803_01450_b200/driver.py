@@ -81,18 +81,34 @@ class Simulation:
     (:mod:`paper_1803_01450_b200.problems`)."""
 
     def __init__(self, problem, device: str = "cuda", stream: torch.cuda.Stream | None = None,
-                 _restore: dict | None = None):
+                 _restore: dict | None = None, reserve_factor: float = 1.0):
+        """``reserve_factor``: after the initial hierarchy is built, warm the
+        device allocator with that multiple of its buffer bytes, so pools
+        that grow at regrids do not pay cudaMalloc inside the time loop
+        (device.reserve)."""
         self._common_init(problem, device, stream)
         if _restore is not None:
             self._restore_from(_restore)
-            return
-        base = self._new_pool(1, boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)]))
-        self._set_initial(base)
-        self.levels[1] = base
-        for lev in range(1, self.L):
-            self._rebuild(lev, init=True)
-        self._mass_prev = self.composite_mass()
-        self.stats.initial_mass = list(self._mass_prev)
+        else:
+            base = self._new_pool(1, boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)]))
+            self._set_initial(base)
+            self.levels[1] = base
+            for lev in range(1, self.L):
+                self._rebuild(lev, init=True)
+            self._mass_prev = self.composite_mass()
+            self.stats.initial_mass = list(self._mass_prev)
+        if reserve_factor > 0:
+            from .device import reserve
+            reserve(int(reserve_factor * self.device_bytes()), self.dev, self.stream)
+
+    def device_bytes(self) -> int:
+        """Bytes of the level pools' state and bathymetry buffers."""
+        n = 0
+        for pool in self.levels.values():
+            for t in list(getattr(pool, "buf", [])) + [getattr(pool, "bathy", None)]:
+                if t is not None:
+                    n += t.numel() * t.element_size()
+        return n
 
     def _common_init(self, problem, device, stream) -> None:
         self.lib = N.lib()
@@ -102,7 +118,10 @@ class Simulation:
         self.specs = [LevelSpec(*s) for s in problem.level_specs()]
         self.L = len(self.specs)
         self.bcs = N.bc_array(problem.boundaries)
-        self.dev = torch.device(device)
+        dev = torch.device(device)
+        if dev.type == "cuda" and dev.index is None:   # recycled buffers compare devices exactly
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
         self.stream = stream or torch.cuda.current_stream(self.dev)
         self.sh = self.stream.cuda_stream
         with torch.cuda.stream(self.stream):
@@ -652,9 +671,10 @@ class Simulation:
         return snap
 
     @classmethod
-    def restore(cls, problem, snap: dict, device: str = "cuda", stream=None) -> "Simulation":
+    def restore(cls, problem, snap: dict, device: str = "cuda", stream=None,
+                reserve_factor: float = 0.0) -> "Simulation":
         """Rebuild a device hierarchy from :meth:`snapshot` output (host->device)."""
-        return cls(problem, device=device, stream=stream, _restore=snap)
+        return cls(problem, device=device, stream=stream, _restore=snap, reserve_factor=reserve_factor)
 
     def _restore_from(self, snap: dict) -> None:
         self.time = snap["time"]

@@ -37,27 +37,38 @@ def cluster_boxes(flags: np.ndarray, efficiency_target: float, allowed=None) -> 
 
 
 _SAT_HOST = {}
+_SAT_DEV = {}
 
 
 def cluster_boxes_device(flags_d, allowed_d, ny: int, nx: int, efficiency_target: float, stream):
     """regrid.cluster_flags from device-resident 0/1 maps: the summed-area
-    tables are exact int32 cumulative sums on the GPU; only the bisection
-    recursion runs on the host (native C++)."""
+    tables are exact int32 sums built on the GPU (``mlamr_sat_u8``); only
+    the bisection recursion runs on the host (native C++)."""
     import torch
     key = (ny, nx)
     if key not in _SAT_HOST:
         _SAT_HOST[key] = (torch.empty((ny + 1) * (nx + 1), dtype=torch.int32, pin_memory=True),
                           torch.empty((ny + 1) * (nx + 1), dtype=torch.int32, pin_memory=True))
     hf, hb = _SAT_HOST[key]
+    dkey = (ny, nx, flags_d.device)
+    if dkey not in _SAT_DEV:
+        with torch.cuda.stream(stream):
+            _SAT_DEV[dkey] = (torch.empty(2 * (ny + 1) * (nx + 1), dtype=torch.int32, device=flags_d.device),
+                              torch.empty(((ny + 31) // 32) * nx, dtype=torch.int32, device=flags_d.device))
+    sat, scratch = _SAT_DEV[dkey]
+    n1 = (ny + 1) * (nx + 1)
+    lib = N.lib()
     with torch.cuda.stream(stream):
-        for src, host, invert in ((flags_d, hf, False), (allowed_d, hb, True)):
-            m = src.view(ny, nx).to(torch.int32)
-            if invert:
-                m = 1 - m
-            sat = torch.zeros((ny + 1, nx + 1), dtype=torch.int32, device=src.device)
-            sat[1:, 1:] = torch.cumsum(torch.cumsum(m, 0, dtype=torch.int32), 1, dtype=torch.int32)
-            host.copy_(sat.view(-1), non_blocking=True)
+        for k, (src, invert) in enumerate(((flags_d, 0), (allowed_d, 1))):
+            N.check(lib.mlamr_sat_u8(src.data_ptr(), ny, nx, invert, sat[k * n1:].data_ptr(), scratch.data_ptr(),
+                                     stream.cuda_stream), "mlamr_sat_u8")
+        hf.copy_(sat[:n1], non_blocking=True)
+        hb.copy_(sat[n1:], non_blocking=True)
     stream.synchronize()
+    return _cluster_from_sat(hf, hb, ny, nx, efficiency_target)
+
+
+def _cluster_from_sat(hf, hb, ny, nx, efficiency_target):
     cap = 4096
     while True:
         out = np.empty((cap, 4), dtype=np.int32)

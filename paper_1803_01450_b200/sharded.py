@@ -42,7 +42,8 @@ _EMPTY = np.zeros((0, 4), np.int64)
 
 
 class ShardedSimulation(Simulation):
-    def __init__(self, problem, comm: Comm | None = None, device: str = "cuda", stream=None):
+    def __init__(self, problem, comm: Comm | None = None, device: str = "cuda", stream=None,
+                 reserve_factor: float = 1.0):
         self.comm = comm or Comm()
         self.rank, self.world = self.comm.rank, self.comm.world
         self.layout, self.owner, self.held = {}, {}, {}
@@ -61,6 +62,9 @@ class ShardedSimulation(Simulation):
             self._rebuild(lev, init=True)
         self._mass_prev = self.composite_mass()
         self.stats.initial_mass = list(self._mass_prev)
+        if reserve_factor > 0:
+            from .device import reserve
+            reserve(int(reserve_factor * self.device_bytes()), self.dev, self.stream)
 
     # -- geometry helpers -----------------------------------------------------
     def _scale(self, level: int):

@@ -1,0 +1,25 @@
+"""mlamr_sat_u8: summed-area tables of 0/1 maps (the clustering's box
+sums, regrid.cluster_flags) equal numpy's cumulative sums exactly."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("ny,nx", [(1, 1), (1, 77), (77, 1), (31, 33), (64, 64), (257, 1000), (1000, 129)])
+@pytest.mark.parametrize("invert", [0, 1])
+def test_sat_equals_cumsum(ny, nx, invert):
+    import torch
+    from paper_1803_01450_b200 import _native as N
+    rng = np.random.default_rng(ny * 1000 + nx + invert)
+    m = (rng.random((ny, nx)) < 0.3).astype(np.uint8)
+    md = torch.from_numpy(m).cuda()
+    sat = torch.full(((ny + 1) * (nx + 1),), -7, dtype=torch.int32, device="cuda")
+    scratch = torch.empty(((ny + 31) // 32) * nx, dtype=torch.int32, device="cuda")
+    N.check(N.lib().mlamr_sat_u8(md.data_ptr(), ny, nx, invert, sat.data_ptr(), scratch.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream), "sat")
+    v = (1 - m.astype(np.int64)) if invert else m.astype(np.int64)
+    ref = np.zeros((ny + 1, nx + 1), np.int64)
+    ref[1:, 1:] = v.cumsum(0).cumsum(1)
+    assert np.array_equal(sat.cpu().numpy().reshape(ny + 1, nx + 1), ref)
