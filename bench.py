@@ -271,6 +271,7 @@ def b200_arm(args):
             dist.barrier()
         t0 = time.perf_counter()
         sim2 = Simulation.restore(pb, snap, stream=stream)
+        Simulation.release_snapshot(snap)   # its pinned buffers take the final snapshot
         c0 = sim2.stats.total_cell_updates
         for _ in range(args.steps):
             coarse_step(sim2)

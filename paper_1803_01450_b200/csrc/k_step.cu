@@ -667,6 +667,13 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
         else
             e = cudaFuncSetAttribute(k_step<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return (int)e;
+#ifdef MLAMR_STEP_CARVEOUT
+        if (y_first)
+            e = cudaFuncSetAttribute(k_step<M, true>, cudaFuncAttributePreferredSharedMemoryCarveout, MLAMR_STEP_CARVEOUT);
+        else
+            e = cudaFuncSetAttribute(k_step<M, false>, cudaFuncAttributePreferredSharedMemoryCarveout, MLAMR_STEP_CARVEOUT);
+        if (e != cudaSuccess) return (int)e;
+#endif
         configured[y_first ? 1 : 0] = true;
     }
     if (n_tiles <= 0) return 0;

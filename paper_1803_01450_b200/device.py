@@ -114,6 +114,30 @@ def release(t: torch.Tensor) -> None:
     del _RECYCLE[16:]
 
 
+# Recycled pinned host buffers for snapshots: cudaHostAlloc costs ~0.5 s per
+# GB, so a snapshot taken inside a timed loop must not allocate.  Buffers
+# are allocated with 50 % slack and handed back by Simulation.release_snapshot.
+_PINNED: list = []
+
+
+def pinned_acquire(numel: int, dtype) -> torch.Tensor:
+    best = None
+    for k, t in enumerate(_PINNED):
+        if t.dtype == dtype and numel <= t.numel() <= 3 * numel + (1 << 20):
+            if best is None or t.numel() < _PINNED[best].numel():
+                best = k
+    if best is not None:
+        return _PINNED.pop(best)[:numel]
+    return torch.empty(int(numel * 1.5) + (1 << 16), dtype=dtype, pin_memory=True)[:numel]
+
+
+def pinned_release(t: torch.Tensor) -> None:
+    base = t._base if t._base is not None else t
+    _PINNED.append(base)
+    _PINNED.sort(key=lambda x: -x.numel())
+    del _PINNED[8:]
+
+
 def reserve(nbytes: int, device, stream) -> None:
     """Warm the caching allocator with ``nbytes`` of device memory.
 

@@ -652,10 +652,11 @@ class Simulation:
                 "stats": replace(self.stats)}
         nbytes = 0
         with torch.cuda.stream(self.stream):
+            from .device import pinned_acquire
             for lev, pool in self.levels.items():
-                st = torch.empty(pool.state.shape, dtype=torch.float64, pin_memory=True)
+                st = pinned_acquire(pool.state.numel(), torch.float64).view(pool.state.shape)
                 st.copy_(pool.state, non_blocking=True)
-                ba = torch.empty(pool.bathy.shape, dtype=torch.float64, pin_memory=True)
+                ba = pinned_acquire(pool.bathy.numel(), torch.float64).view(pool.bathy.shape)
                 ba.copy_(pool.bathy, non_blocking=True)
                 nbytes += st.numel() * 8 + ba.numel() * 8
                 snap["levels"][lev] = {"boxes": pool.boxes.copy(), "state": st, "bathy": ba, "time": pool.time,
@@ -669,6 +670,18 @@ class Simulation:
         snap["nbytes"] = nbytes
         self.d2h_bytes += nbytes
         return snap
+
+    @staticmethod
+    def release_snapshot(snap: dict) -> None:
+        """Hand a snapshot's pinned buffers back for reuse by later
+        snapshots (after any restore from it has been issued: reuse is
+        ordered on the driver stream)."""
+        from .device import pinned_release
+        for d in snap.get("levels", {}).values():
+            for key in ("state", "bathy"):
+                if d.get(key) is not None:
+                    pinned_release(d[key])
+                    d[key] = None
 
     @classmethod
     def restore(cls, problem, snap: dict, device: str = "cuda", stream=None,
