@@ -310,6 +310,7 @@ __global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_le
     const int64_t FF = fine.field_stride, CF = coarse.field_stride;
     const double tol = prm.dry_tolerance;
     const double nblk = (double)(r_x * r_y);
+    const bool vec2 = !((fv.NX | fv.off | FF) & 1);
     double dsum[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) dsum[m] = 0.0;
@@ -328,10 +329,24 @@ __global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_le
                 double s = 0.0;
                 if (RX > 0 && RY > 0) {
                     double v[RY > 0 ? RY : 1][RX > 0 ? RX : 1];
+                    if (RX % 2 == 0 && vec2) {
+                        // even ratios: fine rows of a refined box start on
+                        // even elements of 256-element aligned patches, so a
+                        // block row is RX/2 aligned 16-byte loads
 #pragma unroll
-                    for (int q = 0; q < (RY > 0 ? RY : 1); ++q)
+                        for (int q = 0; q < (RY > 0 ? RY : 1); ++q)
 #pragma unroll
-                        for (int pp = 0; pp < (RX > 0 ? RX : 1); ++pp) v[q][pp] = a[(int64_t)q * fv.NX + pp];
+                            for (int pp = 0; pp < (RX > 0 ? RX : 1); pp += 2) {
+                                const double2 w = *reinterpret_cast<const double2 *>(a + (int64_t)q * fv.NX + pp);
+                                v[q][pp] = w.x;
+                                v[q][pp + 1] = w.y;
+                            }
+                    } else {
+#pragma unroll
+                        for (int q = 0; q < (RY > 0 ? RY : 1); ++q)
+#pragma unroll
+                            for (int pp = 0; pp < (RX > 0 ? RX : 1); ++pp) v[q][pp] = a[(int64_t)q * fv.NX + pp];
+                    }
 #pragma unroll
                     for (int q = 0; q < (RY > 0 ? RY : 1); ++q) {
                         double rs = v[q][0];
