@@ -29,7 +29,7 @@ import ctypes
 import time
 from collections import defaultdict
 from contextlib import contextmanager
-from dataclasses import asdict, dataclass, field, replace
+from dataclasses import asdict, dataclass, field, fields, replace
 
 import numpy as np
 import torch
@@ -66,6 +66,15 @@ class RunStats:
     hyperbolicity_warnings: int = 0
     wet_prefix_repairs: int = 0
     clipped_mass: list = field(default_factory=list)
+
+    @classmethod
+    def from_json(cls, path) -> "RunStats":
+        import json
+        with open(path) as f:
+            data = json.load(f)
+        data["cell_updates_per_level"] = {int(k): int(v) for k, v in data.get("cell_updates_per_level", {}).items()}
+        known = {f.name for f in fields(cls)}
+        return cls(**{k: v for k, v in data.items() if k in known})
 
     def to_json(self, path) -> None:
         import json
