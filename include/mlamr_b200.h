@@ -205,6 +205,16 @@ int mlamr_copy_segments(const double *src, int64_t src_stride, double *dst, int6
                         const int64_t *segments, int n_segments, int max_len, int nplanes,
                         void *stream);
 
+/* Harness Bernoulli flag rule on the device (C5):
+ * flags = dilate^dilate_w(u < p) & covered & allowed and allowed =
+ * erode(covered, 1), with u the splitmix64 counter hash of (seed,
+ * stream_id, j, i) -- bit-identical to problems.hash_uniform -- and covered
+ * read from the level's interior owner map `own` (frame-extended, >= 0 =
+ * covered).  0/1 byte maps [ny][nx]; scratch is 3*ny*nx bytes. */
+int mlamr_flags_bernoulli(const int32_t *own, int ny, int nx, unsigned long long seed,
+                          unsigned long long stream_id, double p, int dilate_w, uint8_t *flags,
+                          uint8_t *allowed, uint8_t *scratch, void *stream);
+
 /* Summed-area table for the clustering bisection (regrid.cluster_flags,
  * regrid.py:129-182): sat is int32 [(ny+1)*(nx+1)] with
  * sat[(j+1)*(nx+1)+(i+1)] = sum over [0,j]x[0,i] of map (invert=0) or

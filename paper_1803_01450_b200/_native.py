@@ -102,6 +102,9 @@ SIGNATURES = {
     "mlamr_step_tile": (ctypes.c_int, [c_vp, c_vp]),
     "mlamr_boxes_meet_any": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
+    "mlamr_flags_bernoulli": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong,
+                                             ctypes.c_ulonglong, ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp,
+                                             c_vp]),
     "mlamr_sat_u8": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_pack_frame": (ctypes.c_int, [Level, c_vp, ctypes.c_int, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
                                         c_vp, c_vp]),

@@ -1086,6 +1086,53 @@ extern "C" int mlamr_flags_reference(const uint8_t *bits, int ny, int nx, int M,
     return (int)cudaGetLastError();
 }
 
+// Harness Bernoulli flag rule (problems.Problem.bernoulli_flags, C5): the
+// counter hash of (seed, stream, j, i) -- splitmix64's finaliser, the same
+// uint64 arithmetic as problems.hash_uniform, so the uniforms are
+// bit-identical to numpy's -- below p flags the cell.  Writes the flag
+// plane and the coverage bits (0x80) of the level's interior owner map.
+__global__ void k_bernoulli(const int32_t *own, int ny, int nx, unsigned long long seed,
+                            unsigned long long stream_id, double p, uint8_t *flag, uint8_t *bits) {
+    const int64_t n = (int64_t)ny * nx;
+    const unsigned long long G = 0x9E3779B97F4A7C15ull, M1 = 0xBF58476D1CE4E5B9ull, M2 = 0x94D049BB133111EBull;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / nx), i = (int)(idx - (int64_t)j * nx);
+        unsigned long long z = seed * G + stream_id * M2 + ((unsigned long long)(long long)j << 32) +
+                               (unsigned long long)(long long)i;
+        z = (z ^ (z >> 30)) * M1;
+        z = (z ^ (z >> 27)) * M2;
+        z = z ^ (z >> 31);
+        const double u = (double)(z >> 11) * (1.0 / 9007199254740992.0);
+        flag[idx] = u < p ? 1 : 0;
+        const bool cov = own[(int64_t)(j + MLAMR_G) * (nx + 2 * MLAMR_G) + (i + MLAMR_G)] >= 0;
+        bits[idx] = cov ? 0x80 : 0;
+    }
+}
+
+// flags = dilate^w(bernoulli) & covered & allowed, allowed = erode(covered, 1)
+// (the driver's host rule for "bernoulli"); scratch is
+// 3*ny*nx bytes.
+extern "C" int mlamr_flags_bernoulli(const int32_t *own, int ny, int nx, unsigned long long seed,
+                                     unsigned long long stream_id, double p, int dilate_w, uint8_t *flags,
+                                     uint8_t *allowed, uint8_t *scratch, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    const int64_t n = (int64_t)ny * nx;
+    if (n <= 0) return 0;
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    uint8_t *a = scratch, *b = scratch + n, *bits = scratch + 2 * n;
+    k_bernoulli<<<nb, 256, 0, st>>>(own, ny, nx, seed, stream_id, p, a, bits);
+    for (int w = 0; w < dilate_w; ++w) {
+        k_morph3<<<nb, 256, 0, st>>>(a, b, ny, nx, 0);
+        uint8_t *t = a; a = b; b = t;
+    }
+    k_covered<<<nb, 256, 0, st>>>(bits, b, n);
+    k_morph3<<<nb, 256, 0, st>>>(b, allowed, ny, nx, 1);
+    k_flag_mask<<<nb, 256, 0, st>>>(a, bits, allowed, n);
+    cudaMemcpyAsync(flags, a, n, cudaMemcpyDeviceToDevice, st);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int mlamr_version(void) { return 1; }
 
 extern "C" const char *mlamr_build_info(void) {

@@ -302,7 +302,7 @@ class Simulation:
         pool = self.levels[level]
         s = self.spec(level)
         rule = self.pb.flag_rule
-        if rule[0] == "reference":
+        if self._device_rule():
             b = self._flag_buffers(level)
             self._device_flags(level)
             with torch.cuda.stream(self.stream):
@@ -333,11 +333,29 @@ class Simulation:
     def flags_for(self, level: int) -> np.ndarray:
         return self.flags_and_allowed(level)[0]
 
+    def _device_rule(self) -> bool:
+        """Flag rules evaluated on the device: the reference rule, and the
+        harness Bernoulli rule (its coverage comes from the level's owner
+        map, which holds every patch on a single GPU)."""
+        return self.pb.flag_rule[0] in ("reference", "bernoulli")
+
     def _device_flags(self, level: int):
-        """Reference flag rule + nesting mask on the device (0/1 byte maps)."""
+        """Flag rule + nesting mask on the device (0/1 byte maps)."""
         pool = self.levels[level]
         s = self.spec(level)
         b = self._flag_buffers(level)
+        if self.pb.flag_rule[0] == "bernoulli":
+            seed = int(self.pb.seed) & 0xFFFFFFFFFFFFFFFF
+            sid = (1000 + 97 * level + 7919 * int(self.steps[level])) & 0xFFFFFFFFFFFFFFFF
+            with torch.cuda.stream(self.stream):
+                self._call(self.lib.mlamr_flags_bernoulli, pool.own.data_ptr(), s.ny, s.nx, seed, sid,
+                           float(self.pb.bernoulli[0]), int(self.pb.flag_rule[2]), b["flags"].data_ptr(),
+                           b["allowed"].data_ptr(), b["scratch"].data_ptr(), self.sh)
+                region = self._region_mask_d(level)
+                if region is not None:
+                    b["flags"].mul_(region)
+                    b["allowed"].mul_(region)
+            return b["flags"], b["allowed"]
         with torch.cuda.stream(self.stream):
             b["bits"].zero_()
             pl, nl = pool.work_list()
@@ -370,7 +388,7 @@ class Simulation:
     def _cluster_level(self, level: int) -> np.ndarray:
         """Coarse boxes of the new finer level (cluster_flags, regrid.py:261)."""
         s = self.spec(level)
-        if self.pb.flag_rule[0] == "reference":
+        if self._device_rule():
             flags_d, allowed_d = self._device_flags(level)
             cb = cluster_boxes_device(flags_d, allowed_d, s.ny, s.nx, self.pb.efficiency_target, self.stream)
             arena().reset()

@@ -200,6 +200,11 @@ class ShardedSimulation(Simulation):
             self.comm.allreduce(wide, dist.ReduceOp.MAX)
             bits.copy_(wide.to(torch.uint8))
 
+    def _device_rule(self) -> bool:
+        # a rank's owner maps hold only its local patches: Bernoulli coverage
+        # comes from the global layout on the host
+        return self.pb.flag_rule[0] == "reference"
+
     def flags_and_allowed(self, level: int):
         s = self.spec(level)
         if self.pb.flag_rule[0] == "bernoulli":

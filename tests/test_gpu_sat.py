@@ -23,3 +23,25 @@ def test_sat_equals_cumsum(ny, nx, invert):
     ref = np.zeros((ny + 1, nx + 1), np.int64)
     ref[1:, 1:] = v.cumsum(0).cumsum(1)
     assert np.array_equal(sat.cpu().numpy().reshape(ny + 1, nx + 1), ref)
+
+
+def test_device_bernoulli_flags_equal_host_rule():
+    """mlamr_flags_bernoulli == the host rule (problems.bernoulli_flags,
+    dilate, coverage, nesting) on a C5-shaped level, several steps."""
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+    from paper_1803_01450_b200.mesh import dilate, paint
+    from paper_1803_01450_b200.regrid import nesting_allowed
+    pb = problems.config5(nx0=64)
+    pb.bernoulli = (0.05,)
+    sim = Simulation(pb)
+    s = sim.spec(1)
+    for step in (0, 1, 7):
+        sim.steps[1] = step
+        flags, allowed = sim.flags_and_allowed(1)
+        covered = paint(sim.levels[1].boxes, s.ny, s.nx)
+        f = dilate(pb.bernoulli_flags(1, step), pb.flag_rule[2]) & covered
+        al = nesting_allowed(sim.levels[1].boxes, s.ny, s.nx)
+        assert np.array_equal(allowed, al)
+        assert np.array_equal(flags, f & al)
+        assert flags.any()
