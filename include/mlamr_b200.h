@@ -81,19 +81,22 @@ int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int32_t *box,
 /* ---- K1: batched patch step (physics.step_patch, physics.py:330-386) -----
  * Reads `src_state` (ghosts filled), writes the stepped interior into
  * `dst_state`.  `tiles` is an int32 [n_tiles*3] work list (patch, j0, i0)
- * of 16x32 interior tiles.  Per-patch observed speeds of the pre-step state
+ * of interior tiles of tile_tx columns (32: 16x32 tiles, 320 threads; 16:
+ * 16x16 tiles, 192 threads, for narrow-patch levels -- see
+ * mlamr_step_tile).  Per-patch observed speeds of the pre-step state
  * go to `speed_bits` (int64 bit patterns, pre-set to -1 = all dry);
  * per-tile partials (sum of clipped negative depth per layer, hyperbolicity
  * fixes, wet-prefix repairs) to `tile_acc` [n_tiles * (M + 2)].
  * Does nothing when *status != 0. */
 int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
-               const int32_t *tiles, int n_tiles, double dt, int y_first,
+               const int32_t *tiles, int n_tiles, int tile_tx, double dt, int y_first,
                mlamr_params prm, long long *speed_bits, double *tile_acc,
                const int32_t *status, void *stream);
 
-/* Interior tile shape (rows, columns) the step kernel was compiled for;
- * the host builds `tiles` with it. */
-int mlamr_step_tile(int *ty, int *tx);
+/* Interior tile shape (rows, columns) the step kernel uses for a level
+ * whose widest patch interior is max_patch_nx cells; the host builds that
+ * level's `tiles` with it and passes tx as tile_tx. */
+int mlamr_step_tile(int max_patch_nx, int *ty, int *tx);
 
 /* CFL guard (physics.py:342-347) + deterministic reduction of a step's
  * partials into acc[M + 2].  A patch whose speed*dt/min(dx,dy) > 1 gets its
@@ -108,7 +111,7 @@ int mlamr_step_finalize(mlamr_level lv, const double *src_state, double *dst_sta
 
 /* ---- K6: per-patch observed max wave speed (physics.py:261-278) --------- */
 int mlamr_max_speed_tiles(mlamr_level lv, const double *state, const int32_t *tiles,
-                          int n_tiles, mlamr_params prm, long long *speed_bits,
+                          int n_tiles, int tile_tx, mlamr_params prm, long long *speed_bits,
                           void *stream);
 
 /* ---- K2: ghost filling (ghost.py:145-197, driver.py:157-190) -------------

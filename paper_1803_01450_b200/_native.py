@@ -62,11 +62,11 @@ SIGNATURES = {
     "mlamr_paint_owner": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int,
                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, c_vp]),
-    "mlamr_step": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_double,
+    "mlamr_step": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                   ctypes.c_int, Params, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_step_finalize": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_double,
                                            Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
-    "mlamr_max_speed_tiles": (ctypes.c_int, [Level, c_vp, c_vp, ctypes.c_int, Params, c_vp, c_vp]),
+    "mlamr_max_speed_tiles": (ctypes.c_int, [Level, c_vp, c_vp, ctypes.c_int, ctypes.c_int, Params, c_vp, c_vp]),
     "mlamr_fill_ghosts": (ctypes.c_int, [Level, ctypes.POINTER(Level), c_vp, ctypes.c_double,
                                          ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp,
                                          ctypes.c_int, c_vp]),
@@ -99,7 +99,7 @@ SIGNATURES = {
                                          ctypes.c_int]),
     "mlamr_chop_boxes": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         c_vp, ctypes.c_int]),
-    "mlamr_step_tile": (ctypes.c_int, [c_vp, c_vp]),
+    "mlamr_step_tile": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp]),
     "mlamr_boxes_meet_any": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_flags_bernoulli": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong,
@@ -135,13 +135,15 @@ def lib():
         fn.restype = res
         fn.argtypes = args
     _lib = L
-    ty, tx = ctypes.c_int(), ctypes.c_int()
-    L.mlamr_step_tile(ctypes.byref(ty), ctypes.byref(tx))
-    STEP_TILE[0], STEP_TILE[1] = ty.value, tx.value
     return L
 
 
-STEP_TILE = [16, 32]
+def step_tile(max_patch_nx: int) -> tuple:
+    """(rows, columns) of the step tiles for a level whose widest patch
+    interior is ``max_patch_nx`` cells (the library picks the shape)."""
+    ty, tx = ctypes.c_int(), ctypes.c_int()
+    lib().mlamr_step_tile(int(max_patch_nx), ctypes.byref(ty), ctypes.byref(tx))
+    return ty.value, tx.value
 
 
 LAUNCHES = [0]

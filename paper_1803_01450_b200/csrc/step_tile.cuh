@@ -1,0 +1,583 @@
+// One tile shape of the batched patch step (K1).  Included by k_step.cu
+// once per shape, inside `namespace mlamr::MLAMR_STEP_NS`, with
+// MLAMR_STEP_TX / _TY (interior tile columns / rows), MLAMR_STEP_NT
+// (threads) and MLAMR_STEP_MINB (CTAs per SM) defined by the includer.
+// Everything shape-dependent lives here: the shared tile, the sweep
+// phases, the step kernel, the tile-based speed kernel and the launcher.
+
+namespace MLAMR_STEP_NS {
+
+constexpr int TX = MLAMR_STEP_TX;
+constexpr int TY = MLAMR_STEP_TY;
+constexpr int PX = TX + 2;
+constexpr int PY = TY + 2;
+constexpr int NPAD = PX * PY;
+constexpr int NFLUX = PY * PX;  // interface (r,c) stored at the cell index of its left/lower cell
+constexpr int NT = MLAMR_STEP_NT;  // threads of the step CTA
+
+template <int M>
+struct StepSmem {
+    double S[3 * M + 1][NPAD];           // h_0..h_{M-1}, hu_.., hv_.., B
+    double cw[NPAD];                     // sqrt(g * max(sum h, 0))
+    double eb[M > 1 ? M - 1 : 1][NPAD];  // eta_{m+1} = B + h_{M-1} + ... + h_{m+1}
+    double u[M][NPAD];                   // normal velocity per layer
+    double v[M][NPAD];                   // transverse velocity per layer
+    double F[2 * M][NFLUX];              // (Fh, Fm) per layer at interface (r,c)-(r,c)+step
+    double src[M > 1 ? M - 1 : 1][NPAD]; // coupling sources of layers 1..M-1
+    double red[(M + 2) * (NT / 32)];
+    long long redi[NT / 32];
+    unsigned char cowet[NPAD];
+    unsigned char wetcol[NPAD];
+};
+
+// All shared-memory phases iterate a rectangle [r0,r1) x [c0,c1) of the
+// padded tile in row-major order with the compile-time row pitch PX, so the
+// index split is a multiply-shift (runtime integer division costs three XU
+// ops and saturated the XU pipe in the first profile) and consecutive
+// threads touch consecutive doubles (no bank conflicts in either sweep
+// direction).
+#define FOR_RECT(r0, r1, c0, c1, ...)                                    \
+    for (int idx_ = threadIdx.x; idx_ < ((r1) - (r0)) * PX; idx_ += NT) { \
+        const int r = (r0) + idx_ / PX;                                  \
+        const int c = idx_ - (idx_ / PX) * PX;                           \
+        if (c < (c0) || c >= (c1)) continue;                             \
+        __VA_ARGS__                                                      \
+    }
+
+
+// Reconstruction bottoms of layer m at a cell (physics.py:200-207, 105-110):
+// co-wet pairs use Zc (0 for upper layers, B for the bottom layer), others
+// Zf (= Bhat: eta_{m+1} for upper layers, B for the bottom layer).
+template <int M>
+__device__ __forceinline__ double zc_of(const StepSmem<M> &s, int m, int k) {
+    return (m == M - 1) ? s.S[3 * M][k] : 0.0;
+}
+template <int M>
+__device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
+    return (m == M - 1) ? s.S[3 * M][k] : s.eb[m < M - 1 ? m : 0][k];
+}
+
+// One directional sweep of all layers over the staged tile
+// (physics._sweep_x / _sweep_y with _layer_inputs), three phases:
+//   A  per cell:      layer inputs (cw, cowet, eta_{m+1}) and velocities
+//   B  per interface: HLL fluxes of every layer, coupling sources
+//   C  per cell:      conservative update + pressure correction + source
+// DIR 0 = x (interfaces between columns c, c+1), 1 = y (rows r, r+1).
+// FIRST: all halo lines (the reference's full=True); else interior lines.
+template <int M, int DIR, bool FIRST>
+__device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
+                           const mlamr_params &prm, const double (&rr)[4][4], double &best) {
+    // lam = dt / d and yd = recip_nr(d) come from the kernel prologue, where
+    // their latency overlaps the tile's in-flight loads
+    const double g = prm.gravity;
+    const double tol = prm.dry_tolerance;
+    const double *B = s.S[3 * M];
+    constexpr int STEP = DIR == 0 ? 1 : PX;  // neighbour offset along the sweep
+    const int n_along = DIR == 0 ? nx2 : ny2;
+    // lines: DIR 0 sweeps rows (lines = rows), DIR 1 sweeps columns
+    const int lr0 = (DIR == 0 && !FIRST) ? 1 : 0, lr1 = (DIR == 0 && !FIRST) ? ny2 - 1 : ny2;
+    const int lc0 = (DIR == 1 && !FIRST) ? 1 : 0, lc1 = (DIR == 1 && !FIRST) ? nx2 - 1 : nx2;
+    // updated cells exclude the first/last cell along the sweep
+    const int ur0 = DIR == 1 ? 1 : lr0, ur1 = DIR == 1 ? ny2 - 1 : lr1;
+    const int uc0 = DIR == 0 ? 1 : lc0, uc1 = DIR == 0 ? nx2 - 1 : lc1;
+    // interfaces: (r,c)-(r,c+1) for DIR 0, (r,c)-(r+1,c) for DIR 1
+    const int fr1 = DIR == 1 ? ny2 - 1 : lr1;
+    const int fc1 = DIR == 0 ? nx2 - 1 : lc1;
+
+    // ---- Phase A: per-cell inputs on the pre-sweep state of this direction
+    FOR_RECT(lr0, lr1, lc0, lc1, {
+        const int k = r * PX + c;
+        double h[M];
+        double hs = 0.0;
+        bool w = true;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            h[m] = s.S[m][k];
+            hs = hs + h[m];
+            w = w && (h[m] > tol);
+        }
+        const double cw = sqrt(g * np_max(hs, 0.0));
+        s.cw[k] = cw;
+        s.cowet[k] = (M == 1) ? 1 : w;
+        if (M > 1) {
+            double e = B[k];
+#pragma unroll
+            for (int m = M - 1; m >= 1; --m) {
+                e = e + h[m];
+                s.eb[m - 1][k] = e;
+            }
+        }
+        const bool interior = FIRST && r >= 1 && r < ny2 - 1 && c >= 1 && c < nx2 - 1 && hs > tol;
+        if (FIRST) s.wetcol[k] = hs > tol;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const bool wet = h[m] > tol;
+            const double hn = s.S[(DIR == 0 ? M : 2 * M) + m][k];
+            const double ht = s.S[(DIR == 0 ? 2 * M : M) + m][k];
+            double u = 0.0, v = 0.0;
+            if (wet) {
+                bool ok = true;
+                const double y = recip_nr(h[m]);
+                u = div_fast(hn, h[m], y, ok);
+                v = div_fast(ht, h[m], y, ok);
+                if (!ok) {
+                    u = hn / h[m];
+                    v = ht / h[m];
+                }
+            }
+            s.u[m][k] = u;
+            s.v[m][k] = v;
+            if (interior) {
+                // observed_max_speed (physics.py:261-278): speed = max(0, x_0,
+                // .., x_{M-1}) + cw with x_m = wet ? max(|hu|/h, |hv|/h) : 0 and
+                // |hu|/h == |hu/h|.  Rounding is monotone, so
+                // max_m(x_m) + cw == max_m(x_m + cw) and 0 + cw == cw: the
+                // running max below is bit-identical to the reference's.
+                const double x = wet ? np_max(fabs(u), fabs(v)) : 0.0;
+                const double cand = (m == 0) ? np_max(cw, x + cw) : x + cw;
+                best = (best < 0.0) ? cand : np_max(best, cand);
+            }
+        }
+    })
+    __syncthreads();
+
+    // ---- Phase B: HLL fluxes per interface (physics.py:101-161) + sources
+    FOR_RECT(lr0, fr1, lc0, fc1, {
+        const int kl = r * PX + c;
+        const int kr = kl + STEP;
+        const bool cop = s.cowet[kl] && s.cowet[kr];
+        const double cl = s.cw[kl];
+        const double cr = s.cw[kr];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const double hl = s.S[m][kl];
+            const double hr = s.S[m][kr];
+            const double Zl = cop ? zc_of<M>(s, m, kl) : zf_of<M>(s, m, kl);
+            const double Zr = cop ? zc_of<M>(s, m, kr) : zf_of<M>(s, m, kr);
+            const double ul = s.u[m][kl];
+            const double ur = s.u[m][kr];
+            const double Zs = Zl > Zr ? Zl : Zr;
+            double hL = (hl + Zl) - Zs;
+            if (hL < 0.0) hL = 0.0;
+            double hR = (hr + Zr) - Zs;
+            if (hR < 0.0) hR = 0.0;
+            double fh = 0.0, fm = 0.0;
+            if (!(hL <= 0.0 && hR <= 0.0)) {
+                const double sl1 = ul - cl, sl2 = ur - cr;
+                const double SL = sl1 < sl2 ? sl1 : sl2;
+                const double sr1 = ul + cl, sr2 = ur + cr;
+                const double SR = sr1 > sr2 ? sr1 : sr2;
+                const double FLh = hL * ul;
+                const double FRh = hR * ur;
+                const double FLm = ((hL * ul) * ul) + (((0.5 * g) * hL) * hL);
+                const double FRm = ((hR * ur) * ur) + (((0.5 * g) * hR) * hR);
+                if (SL >= 0.0) {
+                    fh = FLh;
+                    fm = FLm;
+                } else if (SR <= 0.0) {
+                    fh = FRh;
+                    fm = FRm;
+                } else {
+                    const double den = SR - SL;
+                    double djump;
+                    if (hL > 0.0 && hR > 0.0)
+                        djump = (hr + zf_of<M>(s, m, kr)) - (hl + zf_of<M>(s, m, kl));
+                    else
+                        djump = hR - hL;
+                    const double nh = ((SR * FLh) - (SL * FRh)) + ((SL * SR) * djump);
+                    const double nm = ((SR * FLm) - (SL * FRm)) + ((SL * SR) * ((hR * ur) - (hL * ul)));
+                    bool ok = true;
+                    const double y = recip_nr(den);
+                    fh = div_fast(nh, den, y, ok);
+                    fm = div_fast(nm, den, y, ok);
+                    if (!ok) {
+                        fh = nh / den;
+                        fm = nm / den;
+                    }
+                }
+            }
+            s.F[2 * m][kl] = fh;
+            s.F[2 * m + 1][kl] = fm;
+
+        }
+        // coupling sources of layers >= 1 for the interface's upper cell
+        // (physics.py:208-211), on the pre-sweep state
+        const int a = DIR == 0 ? c : r;
+        if (M > 1 && a + 1 < n_along - 1) {
+            const int k = kr, km = kl, kp = kr + STEP;
+            const bool wm = s.cowet[km] && s.cowet[k];
+            const bool wp = s.cowet[k] && s.cowet[kp];
+#pragma unroll
+            for (int m = 1; m < M; ++m) {
+                double acc = 0.0;
+                bool has = false;
+                bool ok = true;
+                if (m < M - 1) {
+                    const double *f = s.eb[m < M - 1 ? m : 0];
+                    const double dm = wm ? f[k] - f[km] : 0.0;
+                    const double dp = wp ? f[kp] - f[k] : 0.0;
+                    const double num = ((-g) * s.S[m][k]) * (0.5 * (dp + dm));
+                    double q = div_fast(num, d, yd, ok);
+                    if (!ok) q = num / d;
+                    acc = q;
+                    has = true;
+                }
+#pragma unroll
+                for (int kk = 0; kk < m; ++kk) {
+                    const double *f = s.S[kk];
+                    const double dm = wm ? f[k] - f[km] : 0.0;
+                    const double dp = wp ? f[kp] - f[k] : 0.0;
+                    const double num = (((-rr[kk][m]) * g) * s.S[m][k]) * (0.5 * (dp + dm));
+                    ok = true;
+                    double q = div_fast(num, d, yd, ok);
+                    if (!ok) q = num / d;
+                    acc = has ? acc + q : q;
+                    has = true;
+                }
+                s.src[m - 1][k] = acc;
+            }
+        }
+    })
+    __syncthreads();
+
+    // ---- Phase C: conservative update + pressure correction + source
+    FOR_RECT(ur0, ur1, uc0, uc1, {
+        const int k = r * PX + c;
+        const int km = k - STEP, kp = k + STEP;
+        const bool copl = s.cowet[km] && s.cowet[k];
+        const bool copr = s.cowet[k] && s.cowet[kp];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            double *H = s.S[m];
+            double *HN = s.S[(DIR == 0 ? M : 2 * M) + m];
+            double *HT = s.S[(DIR == 0 ? 2 * M : M) + m];
+            const double h0 = H[k];
+            // this cell's reconstructed depths at its two faces: hsR of the
+            // left interface and hsL of the right one (physics.py:113-121)
+            const double Zl_l = copl ? zc_of<M>(s, m, km) : zf_of<M>(s, m, km);
+            const double Zk_l = copl ? zc_of<M>(s, m, k) : zf_of<M>(s, m, k);
+            const double Zk_r = copr ? zc_of<M>(s, m, k) : zf_of<M>(s, m, k);
+            const double Zr_r = copr ? zc_of<M>(s, m, kp) : zf_of<M>(s, m, kp);
+            const double Zs_l = Zl_l > Zk_l ? Zl_l : Zk_l;
+            const double Zs_r = Zk_r > Zr_r ? Zk_r : Zr_r;
+            double hsR_l = (h0 + Zk_l) - Zs_l;
+            if (hsR_l < 0.0) hsR_l = 0.0;
+            double hsL_r = (h0 + Zk_r) - Zs_r;
+            if (hsL_r < 0.0) hsL_r = 0.0;
+            const double fhl = s.F[2 * m][km], fhr = s.F[2 * m][k];
+            const double fml = s.F[2 * m + 1][km], fmr = s.F[2 * m + 1][k];
+            // upwinded transverse flux (physics.py:155-161)
+            const double fvl = fhl > 0.0 ? fhl * s.v[m][km] : (fhl < 0.0 ? fhl * s.v[m][k] : 0.0);
+            const double fvr = fhr > 0.0 ? fhr * s.v[m][k] : (fhr < 0.0 ? fhr * s.v[m][kp] : 0.0);
+            H[k] = h0 - lam * (fhr - fhl);
+            double hn = (HN[k] - lam * (fmr - fml)) - (((lam * 0.5) * g) * ((hsR_l * hsR_l) - (hsL_r * hsL_r)));
+            if (M > 1) {
+                double sm;
+                if (m == 0) {  // physics.py:210, from the pre-sweep eta_1 and own h_0
+                    const double *f = s.eb[0];
+                    const double dm = copl ? f[k] - f[km] : 0.0;
+                    const double dp = copr ? f[kp] - f[k] : 0.0;
+                    const double num = ((-g) * h0) * (0.5 * (dp + dm));
+                    bool ok = true;
+                    sm = div_fast(num, d, yd, ok);
+                    if (!ok) sm = num / d;
+                } else {
+                    sm = s.src[m - 1][k];
+                }
+                hn = hn + dt * sm;
+            }
+            HN[k] = hn;
+            HT[k] = HT[k] - lam * (fvr - fvl);
+        }
+    })
+    __syncthreads();
+}
+
+template <int M, bool YFIRST>
+__global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, const double *__restrict__ src,
+                                             double *__restrict__ dst,
+                                             const int32_t *__restrict__ tiles, double dt,
+                                             mlamr_params prm, StepConst kc, long long *speed_bits,
+                                             double *tile_acc, const int32_t *status) {
+    if (status != nullptr && *status != 0) return;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    StepSmem<M> &s = *reinterpret_cast<StepSmem<M> *>(smem_raw);
+    const int t = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int p = tiles[3 * tile];
+    const int tj0 = tiles[3 * tile + 1];
+    const int ti0 = tiles[3 * tile + 2];
+    const PatchView pv = patch_view(lv, p);
+    const int ty = min(TY, pv.ny - tj0);
+    const int tx = min(TX, pv.nx - ti0);
+    const int ny2 = ty + 2, nx2 = tx + 2;
+    const int64_t FS = lv.field_stride;
+    const int64_t base = pv.off + (int64_t)(tj0 + 1) * pv.NX + (ti0 + 1);
+
+    // stage the padded tile with asynchronous 8-byte copies (LDGSTS): every
+    // thread keeps ~NITEM*(3M+1) global loads in flight instead of
+    // serialising load -> shared store pairs.  The (row, column) split of a
+    // thread's items is done once; each plane then costs one address add and
+    // one LDGSTS per item.
+    {
+        constexpr int NITEM = (NPAD + NT - 1) / NT;
+        unsigned sa[NITEM];
+        const double *ga[NITEM];
+        bool in[NITEM];
+#pragma unroll
+        for (int i = 0; i < NITEM; ++i) {
+            const int idx = t + i * NT;
+            const int r = idx / PX, c = idx - (idx / PX) * PX;
+            in[i] = idx < ny2 * PX && c < nx2;
+            sa[i] = (unsigned)__cvta_generic_to_shared(&s.S[0][0]) + idx * 8;
+            ga[i] = src + base + (int64_t)r * pv.NX + c;
+        }
+        const int64_t boff = lv.bathy - src;  // same patch layout, one plane
+#pragma unroll
+        for (int q = 0; q < 3 * M + 1; ++q) {
+            const int64_t po = (q < 3 * M) ? q * FS : boff;
+#pragma unroll
+            for (int i = 0; i < NITEM; ++i)
+                if (in[i])
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa[i] + q * NPAD * 8),
+                                 "l"(ga[i] + po));
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    const double(&rr)[4][4] = kc.rr;
+    const double lam_x = kc.lam_x, lam_y = kc.lam_y;
+    const double y_x = recip_nr(lv.dx), y_y = recip_nr(lv.dy);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+
+    double best = -1.0;  // running observed speed over this thread's cells
+    if (YFIRST)
+        sweep_tile<M, 1, true>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
+    else
+        sweep_tile<M, 0, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
+
+    if (YFIRST)
+        sweep_tile<M, 0, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
+    else
+        sweep_tile<M, 1, false>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
+
+    // post-processing on the tile interior (physics.py:360-376)
+    const double tol = prm.dry_tolerance;
+    double negs[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) negs[m] = 0.0;
+    long long fixes = 0, repairs = 0;
+    const double coef = kc.coef;
+    FOR_RECT(1, ny2 - 1, 1, nx2 - 1, {
+        const int k = r * PX + c;
+        double h[M], hu[M], hv[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            h[m] = s.S[m][k];
+            hu[m] = s.S[M + m][k];
+            hv[m] = s.S[2 * M + m][k];
+            const double neg = np_min(h[m], 0.0);
+            negs[m] = negs[m] + neg;
+            if (neg < 0.0) h[m] = 0.0;
+        }
+        if (M == 2) {  // _blend_shear (physics.py:292-327)
+            const double h1 = h[0], h2 = h[1 % M];
+            if (h1 > tol && h2 > tol) {
+                const double hu1 = hu[0], hu2 = hu[1 % M], hv1 = hv[0], hv2 = hv[1 % M];
+                bool ok = true;
+                const double y1 = recip_nr(h1), y2 = recip_nr(h2);
+                double u1 = div_fast(hu1, h1, y1, ok), v1 = div_fast(hv1, h1, y1, ok);
+                double u2 = div_fast(hu2, h2, y2, ok), v2 = div_fast(hv2, h2, y2, ok);
+                if (!ok) {
+                    u1 = hu1 / h1;
+                    u2 = hu2 / h2;
+                    v1 = hv1 / h1;
+                    v2 = hv2 / h2;
+                }
+                const double du = u1 - u2, dv = v1 - v2;
+                const double shear2 = (du * du) + (dv * dv);
+                const double bound = coef * (h1 + h2);
+                if (shear2 > bound) {
+                    ++fixes;
+                    const double alpha = sqrt(bound / shear2);
+                    const double htot = h1 + h2;
+                    const double umean = (hu1 + hu2) / htot;
+                    const double vmean = (hv1 + hv2) / htot;
+                    hu[0] = h1 * (umean + alpha * (u1 - umean));
+                    hu[1 % M] = h2 * (umean + alpha * (u2 - umean));
+                    hv[0] = h1 * (vmean + alpha * (v1 - vmean));
+                    hv[1 % M] = h2 * (vmean + alpha * (v2 - vmean));
+                }
+            }
+        }
+        // restore_wet_prefix (state.py:125-145), then zero_dry_momenta (:104-110)
+#pragma unroll
+        for (int m = 1; m < M; ++m) {
+            if (h[m] > tol && h[m - 1] <= tol) {
+                ++repairs;
+                h[m - 1] = h[m - 1] + h[m];
+                hu[m - 1] = hu[m - 1] + hu[m];
+                hv[m - 1] = hv[m - 1] + hv[m];
+                h[m] = 0.0;
+                hu[m] = 0.0;
+                hv[m] = 0.0;
+            }
+        }
+        const int64_t gaddr = base + (int64_t)r * pv.NX + c;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            if (h[m] <= tol) {
+                hu[m] = 0.0;
+                hv[m] = 0.0;
+            }
+            dst[m * FS + gaddr] = h[m];
+            dst[(M + m) * FS + gaddr] = hu[m];
+            dst[(2 * M + m) * FS + gaddr] = hv[m];
+        }
+    })
+    // per-tile partials in one fused pass: warp shuffles (fixed xor tree),
+    // then warp 0 combines the NT/32 warp values in warp order -- the same
+    // order on every run, so the sums are deterministic
+    constexpr int NW = NT / 32;
+    const int lane = t & 31, warp = t >> 5;
+    double v[M + 2];
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = negs[m];
+    v[M] = (double)fixes;
+    v[M + 1] = (double)repairs;
+    // negative-depth sums and counters are zero in almost every warp: the
+    // shuffle tree runs only where one is not
+    bool any = false;
+#pragma unroll
+    for (int q = 0; q < M + 2; ++q) any = any || (v[q] != 0.0);
+    if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+            for (int q = 0; q < M + 2; ++q) v[q] = v[q] + __shfl_xor_sync(0xffffffffu, v[q], off);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < M + 2; ++q) v[q] = 0.0;
+    }
+    // speed max on the bit patterns: speeds are >= 0 (or NaN, canonicalised
+    // above every finite value), and "no wet column" is -1, so the ordering
+    // of the signed 64-bit patterns is the numpy maximum the reference takes
+    const long long mybits = (best < 0.0) ? -1LL
+                           : ((best != best) ? 0x7ff8000000000000LL : __double_as_longlong(best));
+    const int hi = __reduce_max_sync(0xffffffffu, (int)(mybits >> 32));
+    const unsigned lo = __reduce_max_sync(0xffffffffu, ((int)(mybits >> 32) == hi) ? (unsigned)mybits : 0u);
+    if (lane == 0) {
+#pragma unroll
+        for (int q = 0; q < M + 2; ++q) s.red[q * NW + warp] = v[q];
+        s.redi[warp] = (hi < 0) ? -1LL : (long long)(((unsigned long long)(unsigned)hi << 32) | lo);
+    }
+    __syncthreads();
+    if (t == 0) {
+        double *acc = tile_acc + (int64_t)tile * (M + 2);
+        for (int q = 0; q < M + 2; ++q) {
+            double a = s.red[q * NW];
+            for (int w = 1; w < NW; ++w) a = a + s.red[q * NW + w];
+            acc[q] = a;
+        }
+        long long b = s.redi[0];
+        for (int w = 1; w < NW; ++w) b = max(b, s.redi[w]);
+        if (b >= 0) atomicMax(speed_bits + p, b);
+    }
+}
+
+// K6: observed max speed per patch without stepping (stable_dt, level 1 dt).
+template <int M>
+__global__ void __launch_bounds__(NTF) k_max_speed(mlamr_level lv, const double *__restrict__ st,
+                                                  const int32_t *__restrict__ tiles,
+                                                  mlamr_params prm, long long *speed_bits) {
+    __shared__ double red[NTF];
+    const int t = threadIdx.x;
+    const int tile = blockIdx.x;
+    const int p = tiles[3 * tile];
+    const int tj0 = tiles[3 * tile + 1];
+    const int ti0 = tiles[3 * tile + 2];
+    const PatchView pv = patch_view(lv, p);
+    const int ty = min(TY, pv.ny - tj0);
+    const int tx = min(TX, pv.nx - ti0);
+    const int64_t FS = lv.field_stride;
+    const double tol = prm.dry_tolerance;
+    double best = -1.0;
+    bool any = false;
+    for (int idx = t; idx < ty * tx; idx += NTF) {
+        const int r = idx / tx;
+        const int c = idx - r * tx;
+        const int64_t k = pv.off + (int64_t)(tj0 + MLAMR_G + r) * pv.NX + (ti0 + MLAMR_G + c);
+        double hs = 0.0, vel = 0.0;
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const double h = st[m * FS + k];
+            hs = hs + h;
+            const bool wet = h > tol;
+            const double hm = wet ? h : 1.0;
+            const double um = fabs(st[(M + m) * FS + k]) / hm;
+            const double vm = fabs(st[(2 * M + m) * FS + k]) / hm;
+            vel = np_max(vel, wet ? np_max(um, vm) : 0.0);
+        }
+        if (!(hs > tol)) continue;
+        const double sp = vel + sqrt(prm.gravity * np_max(hs, 0.0));
+        best = any ? np_max(best, sp) : sp;
+        any = true;
+    }
+    red[t] = any ? best : -1.0;
+    __syncthreads();
+    for (int s2 = NTF / 2; s2 > 0; s2 >>= 1) {
+        if (t < s2) {
+            const double a = red[t], b = red[t + s2];
+            red[t] = (a < 0.0) ? b : ((b < 0.0) ? a : np_max(a, b));
+        }
+        __syncthreads();
+    }
+    if (t == 0 && !(red[0] < 0.0)) {
+        const double v = red[0];
+        const long long bits = (v != v) ? 0x7ff8000000000000LL : __double_as_longlong(v);
+        atomicMax(speed_bits + p, bits);
+    }
+}
+
+template <int M>
+static int launch_step(const mlamr_level &lv, const double *src, double *dst,
+                       const int32_t *tiles, int n_tiles, double dt, int y_first,
+                       const mlamr_params &prm, long long *speed_bits, double *tile_acc,
+                       const int32_t *status, cudaStream_t st) {
+    const size_t smem = sizeof(StepSmem<M>);
+    static bool configured[2] = {false, false};
+    if (!configured[y_first ? 1 : 0]) {
+        cudaError_t e;
+        if (y_first)
+            e = cudaFuncSetAttribute(k_step<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        else
+            e = cudaFuncSetAttribute(k_step<M, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return (int)e;
+#ifdef MLAMR_STEP_CARVEOUT
+        if (y_first)
+            e = cudaFuncSetAttribute(k_step<M, true>, cudaFuncAttributePreferredSharedMemoryCarveout, MLAMR_STEP_CARVEOUT);
+        else
+            e = cudaFuncSetAttribute(k_step<M, false>, cudaFuncAttributePreferredSharedMemoryCarveout, MLAMR_STEP_CARVEOUT);
+        if (e != cudaSuccess) return (int)e;
+#endif
+        configured[y_first ? 1 : 0] = true;
+    }
+    if (n_tiles <= 0) return 0;
+    StepConst kc;
+    kc.lam_x = dt / lv.dx;
+    kc.lam_y = dt / lv.dy;
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b)
+            kc.rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
+    kc.coef = (M > 1) ? prm.gravity * (1.0 - kc.rr[0][1]) : 0.0;
+    if (y_first)
+        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status);
+    else
+        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status);
+    return (int)cudaGetLastError();
+}
+
+#undef FOR_RECT
+
+}  // namespace MLAMR_STEP_NS

@@ -165,12 +165,14 @@ def arena() -> PinnedArena:
     return _ARENA
 
 
-def tile_list(boxes: np.ndarray) -> np.ndarray:
-    """(patch, j0, i0) for every step tile (shape from the library), patch-major."""
-    N.lib()
-    TILE_Y, TILE_X = N.STEP_TILE
+def tile_list(boxes: np.ndarray, shape: Optional[tuple] = None) -> np.ndarray:
+    """(patch, j0, i0) for every step tile, patch-major; ``shape`` = (rows,
+    columns), by default the library's choice for these boxes."""
     if len(boxes) == 0:
         return np.zeros((0, 3), np.int32)
+    if shape is None:
+        shape = N.step_tile(int((boxes[:, 2] - boxes[:, 0] + 1).max()))
+    TILE_Y, TILE_X = shape
     nx = boxes[:, 2] - boxes[:, 0] + 1
     ny = boxes[:, 3] - boxes[:, 1] + 1
     tx = (nx + TILE_X - 1) // TILE_X
@@ -232,7 +234,9 @@ class LevelPool:
             self.off_d = A.upload(self.offsets, device, stream)
             _t3 = _t.perf_counter()
             _p["upload"] += _t3 - _t2
-            tl = tile_list(b)
+            self.tile_shape = N.step_tile(int((b[:, 2] - b[:, 0] + 1).max()) if self.P else 0)
+            self.tile_tx = self.tile_shape[1]
+            tl = tile_list(b, self.tile_shape)
             _p["tile_list"] += _t.perf_counter() - _t3
             if self.owned is not None and len(tl):
                 tl = tl[self.owned[tl[:, 0]]]

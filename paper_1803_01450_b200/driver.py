@@ -501,7 +501,7 @@ class Simulation:
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
         self._call(self.lib.mlamr_step, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
-                   pool.n_tiles, dt, y_first, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
+                   pool.n_tiles, pool.tile_tx, dt, y_first, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
                    self.status.data_ptr(), self.sh)
         if timed:
             e1.record(self.stream)
@@ -559,7 +559,7 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             pool.speed_bits.fill_(-1)
         self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(), pool.tiles_d.data_ptr(),
-                   pool.n_tiles, self.prm, pool.speed_bits.data_ptr(), self.sh)
+                   pool.n_tiles, pool.tile_tx, self.prm, pool.speed_bits.data_ptr(), self.sh)
         self.stream.synchronize()
         self.d2h_bytes += 8 * pool.P
         bits = pool.speed_bits[:pool.P].cpu().numpy()

@@ -91,7 +91,7 @@ def observed_max_speed(patch, params) -> float:
     pool = _pool_for([patch], b.hi_i + 1, b.hi_j + 1, dx, dy, M)
     L = N.lib()
     N.check(L.mlamr_max_speed_tiles(pool.struct(), pool.state.data_ptr(), pool.tiles_d.data_ptr(),
-                                    pool.n_tiles, _params(params), pool.speed_bits.data_ptr(),
+                                    pool.n_tiles, pool.tile_tx, _params(params), pool.speed_bits.data_ptr(),
                                     torch.cuda.current_stream().cuda_stream), "max_speed")
     bits = int(pool.speed_bits[0].item())
     return 0.0 if bits < 0 else float(np.array([bits], np.int64).view(np.float64)[0])
@@ -120,7 +120,7 @@ def step_patch(patch, dt: float, params, y_first: bool = False) -> StepResult:
     src, dst = pool.state, pool.other
     dst.copy_(src)  # ghost frame of the result = input frame
     lv = pool.struct(src)
-    N.check(L.mlamr_step(lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(), pool.n_tiles, dt,
+    N.check(L.mlamr_step(lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(), pool.n_tiles, pool.tile_tx, dt,
                          int(bool(y_first)), prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
                          status.data_ptr(), sh), "step")
     N.check(L.mlamr_step_finalize(lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(), pool.n_tiles,

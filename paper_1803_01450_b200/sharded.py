@@ -172,7 +172,8 @@ class ShardedSimulation(Simulation):
                 pool.speed_bits.fill_(-1)
                 if pool.n_tiles:
                     self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(),
-                               pool.tiles_d.data_ptr(), pool.n_tiles, self.prm, pool.speed_bits.data_ptr(),
+                               pool.tiles_d.data_ptr(), pool.n_tiles, pool.tile_tx, self.prm,
+                               pool.speed_bits.data_ptr(),
                                self.sh)
                 best = torch.max(pool.speed_bits[:pool.P]).reshape(1)
             self.comm.allreduce(best, dist.ReduceOp.MAX if self.world > 1 else None)
