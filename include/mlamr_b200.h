@@ -218,6 +218,18 @@ int mlamr_flags_bernoulli(const int32_t *own, int ny, int nx, unsigned long long
                           unsigned long long stream_id, double p, int dilate_w, uint8_t *flags,
                           uint8_t *allowed, uint8_t *scratch, void *stream);
 
+/* Harness gradient flag rule on the device (C1/C3): with
+ * eta_m = (h_{M-1} + ... + h_m) + B of the layers in layer_mask on the
+ * level grid (interior owner wins), a covered cell is flagged when
+ * |eta difference| / spacing across a face shared with another covered
+ * cell exceeds tol in any of those layers; then flags = dilate^dilate_w &
+ * covered & allowed, allowed = erode(covered, 1).  0/1 byte maps
+ * [ny][nx]; scratch 3*ny*nx bytes, eta_scratch popcount(layer_mask)*ny*nx
+ * doubles. */
+int mlamr_flags_gradient(mlamr_level lv, const double *state, mlamr_params prm, unsigned layer_mask,
+                         double tol, int dilate_w, uint8_t *flags, uint8_t *allowed, uint8_t *scratch,
+                         double *eta_scratch, void *stream);
+
 /* Summed-area table for the clustering bisection (regrid.cluster_flags,
  * regrid.py:129-182): sat is int32 [(ny+1)*(nx+1)] with
  * sat[(j+1)*(nx+1)+(i+1)] = sum over [0,j]x[0,i] of map (invert=0) or

@@ -105,6 +105,8 @@ SIGNATURES = {
     "mlamr_flags_bernoulli": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong,
                                              ctypes.c_ulonglong, ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp,
                                              c_vp]),
+    "mlamr_flags_gradient": (ctypes.c_int, [Level, c_vp, Params, ctypes.c_uint, ctypes.c_double, ctypes.c_int,
+                                            c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_sat_u8": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_pack_frame": (ctypes.c_int, [Level, c_vp, ctypes.c_int, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
                                         c_vp, c_vp]),

@@ -1133,6 +1133,98 @@ extern "C" int mlamr_flags_bernoulli(const int32_t *own, int ny, int nx, unsigne
     return (int)cudaGetLastError();
 }
 
+// Harness gradient flag rule (problems.gradient_flags_map, C1/C3).  Stage 1:
+// the surfaces eta_m = (h_{M-1} + ... + h_m) + B (numpy's reversed cumsum,
+// driver.level_surfaces) of the requested layers on the level grid, from
+// the interior owner (later patches win, as the host's overwrite), and the
+// coverage bit.  Stage 2: a covered cell is flagged when |difference| /
+// spacing across one of its faces with another covered cell exceeds tol.
+template <int M>
+__global__ void k_grad_eta(mlamr_level lv, const double *__restrict__ state, unsigned layer_mask,
+                           double *__restrict__ eta, uint8_t *__restrict__ bits) {
+    const int ny = lv.level_ny, nx = lv.level_nx;
+    const int64_t n = (int64_t)ny * nx;
+    const int64_t FS = lv.field_stride;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / nx), i = (int)(idx - (int64_t)j * nx);
+        const int o = owner_at(lv.own, nx, ny, i, j);
+        if (o < 0) {
+            bits[idx] = 0;
+            continue;
+        }
+        bits[idx] = 0x80;
+        const PatchView pv = patch_view(lv, o);
+        const int64_t k = pv.off + (int64_t)(j - pv.lo_j + MLAMR_G) * pv.NX + (i - pv.lo_i + MLAMR_G);
+        const double B = lv.bathy[k];
+        double c = state[(M - 1) * FS + k];
+        int slot = 0;
+        double e[M];
+        e[M - 1] = c + B;
+#pragma unroll
+        for (int m = M - 2; m >= 0; --m) {
+            c = c + state[m * FS + k];
+            e[m] = c + B;
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m)
+            if (layer_mask & (1u << m)) eta[(int64_t)(slot++) * n + idx] = e[m];
+    }
+}
+
+__global__ void k_grad_flags(const double *__restrict__ eta, int K, const uint8_t *__restrict__ bits, int ny,
+                             int nx, double dx, double dy, double tol, uint8_t *__restrict__ flag) {
+    const int64_t n = (int64_t)ny * nx;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / nx), i = (int)(idx - (int64_t)j * nx);
+        bool f = false;
+        if (bits[idx] & 0x80) {
+            const bool cl = i > 0 && (bits[idx - 1] & 0x80), cr = i + 1 < nx && (bits[idx + 1] & 0x80);
+            const bool cb = j > 0 && (bits[idx - nx] & 0x80), ct = j + 1 < ny && (bits[idx + nx] & 0x80);
+            for (int q = 0; q < K; ++q) {
+                const double *e = eta + (int64_t)q * n;
+                const double v = e[idx];
+                if (cl && fabs(v - e[idx - 1]) / dx > tol) f = true;
+                if (cr && fabs(e[idx + 1] - v) / dx > tol) f = true;
+                if (cb && fabs(v - e[idx - nx]) / dy > tol) f = true;
+                if (ct && fabs(e[idx + nx] - v) / dy > tol) f = true;
+            }
+        }
+        flag[idx] = f ? 1 : 0;
+    }
+}
+
+// flags = dilate^w(gradient flags) & covered & allowed, allowed =
+// erode(covered, 1) (the driver's host rule for "gradient"); eta_scratch
+// holds popcount(layer_mask) level-sized fp64 planes, scratch 3*ny*nx bytes.
+extern "C" int mlamr_flags_gradient(mlamr_level lv, const double *state, mlamr_params prm, unsigned layer_mask,
+                                    double tol, int dilate_w, uint8_t *flags, uint8_t *allowed, uint8_t *scratch,
+                                    double *eta_scratch, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    const int ny = lv.level_ny, nx = lv.level_nx;
+    const int64_t n = (int64_t)ny * nx;
+    if (n <= 0) return 0;
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    uint8_t *a = scratch, *b = scratch + n, *bits = scratch + 2 * n;
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_grad_eta<M><<<nb, 256, 0, st>>>(lv, state, layer_mask, eta_scratch, bits);
+    });
+    if (rc) return rc;
+    const int K = __builtin_popcount(layer_mask & ((1u << prm.num_layers) - 1u));
+    k_grad_flags<<<nb, 256, 0, st>>>(eta_scratch, K, bits, ny, nx, lv.dx, lv.dy, tol, a);
+    for (int w = 0; w < dilate_w; ++w) {
+        k_morph3<<<nb, 256, 0, st>>>(a, b, ny, nx, 0);
+        uint8_t *t = a; a = b; b = t;
+    }
+    k_covered<<<nb, 256, 0, st>>>(bits, b, n);
+    k_morph3<<<nb, 256, 0, st>>>(b, allowed, ny, nx, 1);
+    k_flag_mask<<<nb, 256, 0, st>>>(a, bits, allowed, n);
+    cudaMemcpyAsync(flags, a, n, cudaMemcpyDeviceToDevice, st);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int mlamr_version(void) { return 1; }
 
 extern "C" const char *mlamr_build_info(void) {

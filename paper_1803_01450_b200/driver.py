@@ -337,13 +337,32 @@ class Simulation:
         """Flag rules evaluated on the device: the reference rule, and the
         harness Bernoulli rule (its coverage comes from the level's owner
         map, which holds every patch on a single GPU)."""
-        return self.pb.flag_rule[0] in ("reference", "bernoulli")
+        return self.pb.flag_rule[0] in ("reference", "bernoulli", "gradient")
 
     def _device_flags(self, level: int):
         """Flag rule + nesting mask on the device (0/1 byte maps)."""
         pool = self.levels[level]
         s = self.spec(level)
         b = self._flag_buffers(level)
+        if self.pb.flag_rule[0] == "gradient":
+            _, tol, width, layers = self.pb.flag_rule
+            mask = 0
+            for m in layers:
+                mask |= 1 << int(m)
+            key = ("eta", level)
+            if key not in self._flagbuf:
+                with torch.cuda.stream(self.stream):
+                    self._flagbuf[key] = torch.empty(len(layers) * s.ny * s.nx, dtype=torch.float64,
+                                                     device=self.dev)
+            with torch.cuda.stream(self.stream):
+                self._call(self.lib.mlamr_flags_gradient, pool.struct(), pool.state.data_ptr(), self.prm, mask,
+                           float(tol), int(width), b["flags"].data_ptr(), b["allowed"].data_ptr(),
+                           b["scratch"].data_ptr(), self._flagbuf[key].data_ptr(), self.sh)
+                region = self._region_mask_d(level)
+                if region is not None:
+                    b["flags"].mul_(region)
+                    b["allowed"].mul_(region)
+            return b["flags"], b["allowed"]
         if self.pb.flag_rule[0] == "bernoulli":
             seed = int(self.pb.seed) & 0xFFFFFFFFFFFFFFFF
             sid = (1000 + 97 * level + 7919 * int(self.steps[level])) & 0xFFFFFFFFFFFFFFFF

@@ -45,3 +45,31 @@ def test_device_bernoulli_flags_equal_host_rule():
         assert np.array_equal(allowed, al)
         assert np.array_equal(flags, f & al)
         assert flags.any()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_device_gradient_flags_equal_host_rule(name):
+    """mlamr_flags_gradient == the host rule (level surfaces,
+    problems.gradient_flags_map, dilate, coverage, nesting)."""
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+    from paper_1803_01450_b200.mesh import dilate
+    from paper_1803_01450_b200.problems import gradient_flags_map
+    from paper_1803_01450_b200.regrid import nesting_allowed
+    pb = problems.config1() if name == "C1" else problems.config3(nx0=32)
+    sim = Simulation(pb)
+    sim.advance_coarse_step(sim.choose_dt())
+    _, tol, width, layers = pb.flag_rule
+    checked = 0
+    for lev in range(1, sim.L):
+        if lev not in sim.levels or sim.levels[lev].P == 0:
+            continue
+        s = sim.spec(lev)
+        flags, allowed = sim.flags_and_allowed(lev)
+        eta, covered = sim.level_surfaces(lev, layers)
+        f = dilate(gradient_flags_map(eta, covered, s.dx, s.dy, tol), width) & covered
+        al = nesting_allowed(sim.levels[lev].boxes, s.ny, s.nx)
+        assert np.array_equal(allowed, al), lev
+        assert np.array_equal(flags, f & al), lev
+        checked += int(flags.sum())
+    assert checked > 0
