@@ -94,9 +94,9 @@ int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                const int32_t *status, void *stream);
 
 /* Interior tile shape (rows, columns) the step kernel uses for a level
- * whose widest patch interior is max_patch_nx cells; the host builds that
- * level's `tiles` with it and passes tx as tile_tx. */
-int mlamr_step_tile(int max_patch_nx, int *ty, int *tx);
+ * whose widest patch interior is max_patch_nx cells and num_layers layers;
+ * the host builds that level's `tiles` with it and passes tx as tile_tx. */
+int mlamr_step_tile(int max_patch_nx, int num_layers, int *ty, int *tx);
 
 /* CFL guard (physics.py:342-347) + deterministic reduction of a step's
  * partials into acc[M + 2].  A patch whose speed*dt/min(dx,dy) > 1 gets its

@@ -99,7 +99,7 @@ SIGNATURES = {
                                          ctypes.c_int]),
     "mlamr_chop_boxes": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         c_vp, ctypes.c_int]),
-    "mlamr_step_tile": (ctypes.c_int, [ctypes.c_int, c_vp, c_vp]),
+    "mlamr_step_tile": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
     "mlamr_boxes_meet_any": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_flags_bernoulli": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong,
@@ -140,11 +140,11 @@ def lib():
     return L
 
 
-def step_tile(max_patch_nx: int) -> tuple:
+def step_tile(max_patch_nx: int, num_layers: int) -> tuple:
     """(rows, columns) of the step tiles for a level whose widest patch
     interior is ``max_patch_nx`` cells (the library picks the shape)."""
     ty, tx = ctypes.c_int(), ctypes.c_int()
-    lib().mlamr_step_tile(int(max_patch_nx), ctypes.byref(ty), ctypes.byref(tx))
+    lib().mlamr_step_tile(int(max_patch_nx), int(num_layers), ctypes.byref(ty), ctypes.byref(tx))
     return ty.value, tx.value
 
 

@@ -152,8 +152,11 @@ __global__ void __launch_bounds__(NTF) k_step_finalize(mlamr_level lv, const dou
 
 using namespace mlamr;
 
-extern "C" int mlamr_step_tile(int max_patch_nx, int *ty, int *tx) {
-    if (max_patch_nx > 0 && max_patch_nx <= narrow::TX) {
+extern "C" int mlamr_step_tile(int max_patch_nx, int num_layers, int *ty, int *tx) {
+    // narrow tiles for narrow patches, and for M >= 3, whose 3M+1 state
+    // planes and per-layer scratch make a wide tile's shared memory
+    // (~132 KB) allow one CTA per SM (narrow: ~70 KB, 3 CTAs)
+    if ((max_patch_nx > 0 && max_patch_nx <= narrow::TX) || num_layers >= 3) {
         *ty = narrow::TY;
         *tx = narrow::TX;
     } else {

@@ -171,7 +171,7 @@ def tile_list(boxes: np.ndarray, shape: Optional[tuple] = None) -> np.ndarray:
     if len(boxes) == 0:
         return np.zeros((0, 3), np.int32)
     if shape is None:
-        shape = N.step_tile(int((boxes[:, 2] - boxes[:, 0] + 1).max()))
+        shape = N.step_tile(int((boxes[:, 2] - boxes[:, 0] + 1).max()), 2)
     TILE_Y, TILE_X = shape
     nx = boxes[:, 2] - boxes[:, 0] + 1
     ny = boxes[:, 3] - boxes[:, 1] + 1
@@ -234,7 +234,7 @@ class LevelPool:
             self.off_d = A.upload(self.offsets, device, stream)
             _t3 = _t.perf_counter()
             _p["upload"] += _t3 - _t2
-            self.tile_shape = N.step_tile(int((b[:, 2] - b[:, 0] + 1).max()) if self.P else 0)
+            self.tile_shape = N.step_tile(int((b[:, 2] - b[:, 0] + 1).max()) if self.P else 0, M)
             self.tile_tx = self.tile_shape[1]
             tl = tile_list(b, self.tile_shape)
             _p["tile_list"] += _t.perf_counter() - _t3

@@ -144,6 +144,7 @@ class Simulation:
             self._eta_rest = torch.tensor(list(problem.eta_rest), dtype=torch.float64, device=self.dev)
             self._wave_tol = torch.tensor(list(problem.wave_tolerance), dtype=torch.float64, device=self.dev)
         self._flagbuf = {}
+        self._scratch_bufs = {}
         self.levels: dict[int, LevelPool] = {}
         self.steps = {s.level: 0 for s in self.specs}
         self._stash = {}
@@ -164,6 +165,22 @@ class Simulation:
             yield
         finally:
             self.host_prof[name] += time.perf_counter() - t0
+
+    def _scratch(self, name: str, n: int, zero: bool = True) -> torch.Tensor:
+        """A float64 device buffer of >= n elements kept across calls (grown
+        by half when too small): per-block partial sums are allocated every
+        step and regrid, and fresh allocations there occasionally reached
+        cudaMalloc inside the time loop.  Reuse is ordered on the stream."""
+        buf = self._scratch_bufs.get(name)
+        if buf is None or buf.numel() < n:
+            with torch.cuda.stream(self.stream):
+                buf = torch.empty(max(int(n * 1.5), 1024), dtype=torch.float64, device=self.dev)
+            self._scratch_bufs[name] = buf
+        out = buf[:max(n, 1)]
+        if zero:
+            with torch.cuda.stream(self.stream):
+                out.zero_()
+        return out
 
     def spec(self, level: int) -> LevelSpec:
         return self.specs[level - 1]
@@ -214,7 +231,7 @@ class Simulation:
             return torch.zeros(self.M, dtype=torch.float64, device=self.dev)
         bpp = pool.blocks_per_patch(pool.max_cells)
         with torch.cuda.stream(self.stream):
-            part = torch.zeros(pool.P * bpp * self.M, dtype=torch.float64, device=self.dev)
+            part = self._scratch("reduce", pool.P * bpp * self.M)
             ghosts = pool.state if pool.ghosts_in_cur else pool.other
             child = pool.child.data_ptr() if pool.child is not None else None
             pl, nl = pool.work_list()
@@ -456,7 +473,7 @@ class Simulation:
                 self._set_initial(new)
             elif new.P:
                 bpp = new.blocks_per_patch(new.max_interior // (rx * ry))
-                part = torch.zeros(new.P * bpp * M, dtype=torch.float64, device=self.dev)
+                part = self._scratch("refine", new.P * bpp * M)
                 fs = self.spec(level + 1)
                 ol = old.struct() if old is not None else empty_level_struct(fs, M)
                 pl, nl = new.work_list()
@@ -467,7 +484,7 @@ class Simulation:
             new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
             if old is not None and old.P and not init:
                 bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
-                part = torch.zeros(old.P * bpp * M, dtype=torch.float64, device=self.dev)
+                part = self._scratch("derefine", old.P * bpp * M)
                 pl, nl = old.work_list()
                 self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
                            rx, ry, self.prm, part.data_ptr(), bpp, pl, nl, self.sh)
@@ -543,7 +560,7 @@ class Simulation:
         s = self.spec(level)
         bpp = fine.blocks_per_patch(fine.max_interior // (s.r_x * s.r_y))
         with torch.cuda.stream(self.stream):
-            part = torch.empty(fine.P * bpp * self.M, dtype=torch.float64, device=self.dev)
+            part = self._scratch("coarsen", fine.P * bpp * self.M, zero=False)
         self._call(self.lib.mlamr_average_down, fine.struct(), coarse.struct(), s.r_x, s.r_y, self.prm,
                    part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
         self._part_keep = part
