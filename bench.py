@@ -201,6 +201,8 @@ def b200_arm(args):
 
     # ---- timed region: K coarse steps, device clock ----------------------
     sim.host_prof.clear()
+    from paper_1803_01450_b200 import device as _D
+    _D.POOL_PROF.clear()
     sim.step_timer_level = L
     sim.step_events = []
     launches0 = N.LAUNCHES[0]
@@ -240,6 +242,8 @@ def b200_arm(args):
         dist.all_reduce(cc, op=dist.ReduceOp.SUM)
         cells_all = float(cc.item())
     value = cells_all / (t_max * 1e-3)
+    if os.environ.get("MLAMR_POOL_PROF"):
+        print("pool_prof_ms", {k: round(1e3 * v, 2) for k, v in _D.POOL_PROF.items()}, file=sys.stderr)
 
     # ---- roofline of the dominant kernel (finest-level step) --------------
     durs, byts = [], []

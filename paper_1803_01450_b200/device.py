@@ -155,7 +155,12 @@ def reserve(nbytes: int, device, stream) -> None:
         return
     with torch.cuda.stream(stream):
         t = torch.empty(n, dtype=torch.uint8, device=device)
-    del t
+        # allocations <= 1 MB come from the allocator's separate small pool
+        # (2 MB segments): warm it too, or patch tables and partial-sum
+        # buffers of a new pool occasionally reach cudaMalloc, which waits
+        # for the queued steps and stalls the regrid by ~100 ms
+        small = [torch.empty(1 << 19, dtype=torch.uint8, device=device) for _ in range(256)]
+    del t, small
 
 
 def arena() -> PinnedArena:
@@ -243,7 +248,9 @@ class LevelPool:
             self.tiles = tl
             self.n_tiles = len(tl)
             self.tiles_d = A.upload(tl, device, stream) if len(tl) else torch.zeros(3, dtype=torch.int32, device=device)
+            _t5 = _t.perf_counter()
             self.tile_acc = torch.zeros(max(self.n_tiles, 1) * (M + 2), dtype=torch.float64, device=device)
+            _p["tile_acc"] += _t.perf_counter() - _t5
             self.owned_d = None
             self.n_owned = self.P
             if self.owned is not None:
