@@ -87,11 +87,17 @@ int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int32_t *box,
  * go to `speed_bits` (int64 bit patterns, pre-set to -1 = all dry);
  * per-tile partials (sum of clipped negative depth per layer, hyperbolicity
  * fixes, wet-prefix repairs) to `tile_acc` [n_tiles * (M + 2)].
+ * With a ghost plan (mlamr_ghost_plan's ghost_base/ghost_plan; NULL = read
+ * the patch's own ghost frame), halo cells that have a sibling source are
+ * read from the sibling's interior directly, so the sibling copy of the
+ * ghost fill need not run for this level (patches that need physical BCs
+ * excepted: their BC corners read the copied frame).
  * Does nothing when *status != 0. */
 int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                const int32_t *tiles, int n_tiles, int tile_tx, double dt, int y_first,
                mlamr_params prm, long long *speed_bits, double *tile_acc,
-               const int32_t *status, void *stream);
+               const int32_t *status, const int64_t *ghost_base, const int64_t *ghost_plan,
+               void *stream);
 
 /* Interior tile shape (rows, columns) the step kernel uses for a level
  * whose widest patch interior is max_patch_nx cells and num_layers layers;

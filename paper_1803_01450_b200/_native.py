@@ -63,7 +63,7 @@ SIGNATURES = {
                                          ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                          ctypes.c_int, c_vp]),
     "mlamr_step": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double,
-                                  ctypes.c_int, Params, c_vp, c_vp, c_vp, c_vp]),
+                                  ctypes.c_int, Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_step_finalize": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_double,
                                            Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_max_speed_tiles": (ctypes.c_int, [Level, c_vp, c_vp, ctypes.c_int, ctypes.c_int, Params, c_vp, c_vp]),

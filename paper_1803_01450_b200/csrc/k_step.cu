@@ -170,23 +170,28 @@ template <int M>
 static int launch_step_shape(int tile_tx, const mlamr_level &lv, const double *src, double *dst,
                              const int32_t *tiles, int n_tiles, double dt, int y_first,
                              const mlamr_params &prm, long long *speed_bits, double *tile_acc,
-                             const int32_t *status, cudaStream_t st) {
+                             const int32_t *status, const int64_t *gbase, const int64_t *gplan,
+                             cudaStream_t st) {
     if (tile_tx == narrow::TX)
-        return narrow::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, st);
+        return narrow::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
+                                      gbase, gplan, st);
     if (tile_tx == wide::TX)
-        return wide::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, st);
+        return wide::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
+                                    gbase, gplan, st);
     return -3;
 }
 
 extern "C" int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                           const int32_t *tiles, int n_tiles, int tile_tx, double dt, int y_first,
                           mlamr_params prm, long long *speed_bits, double *tile_acc,
-                          const int32_t *status, void *stream) {
+                          const int32_t *status, const int64_t *ghost_base, const int64_t *ghost_plan,
+                          void *stream) {
     cudaStream_t st = as_stream(stream);
+    const int64_t *gb = ghost_plan ? ghost_base : nullptr;
     switch (prm.num_layers) {
-        case 1: return launch_step_shape<1>(tile_tx, lv, src_state, dst_state, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, st);
-        case 2: return launch_step_shape<2>(tile_tx, lv, src_state, dst_state, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, st);
-        case 3: return launch_step_shape<3>(tile_tx, lv, src_state, dst_state, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, st);
+        case 1: return launch_step_shape<1>(tile_tx, lv, src_state, dst_state, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, gb, ghost_plan, st);
+        case 2: return launch_step_shape<2>(tile_tx, lv, src_state, dst_state, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, gb, ghost_plan, st);
+        case 3: return launch_step_shape<3>(tile_tx, lv, src_state, dst_state, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status, gb, ghost_plan, st);
         default: return -1;
     }
 }

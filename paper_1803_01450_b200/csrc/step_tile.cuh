@@ -298,7 +298,9 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
                                              double *__restrict__ dst,
                                              const int32_t *__restrict__ tiles, double dt,
                                              mlamr_params prm, StepConst kc, long long *speed_bits,
-                                             double *tile_acc, const int32_t *status) {
+                                             double *tile_acc, const int32_t *status,
+                                             const int64_t *__restrict__ gbase,
+                                             const int64_t *__restrict__ gplan) {
     if (status != nullptr && *status != 0) return;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StepSmem<M> &s = *reinterpret_cast<StepSmem<M> *>(smem_raw);
@@ -331,6 +333,25 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
             in[i] = idx < ny2 * PX && c < nx2;
             sa[i] = (unsigned)__cvta_generic_to_shared(&s.S[0][0]) + idx * 8;
             ga[i] = src + base + (int64_t)r * pv.NX + c;
+            if (gplan != nullptr && in[i]) {
+                // halo cell in the patch's ghost frame: with a ghost plan the
+                // sibling copy is fused into this staging -- read the covering
+                // sibling's interior cell directly (ghost.py:186-196); cells
+                // without a sibling (coarse interpolation, physical BC) come
+                // from the frame the fill kernels wrote
+                const int J = tj0 + 1 + r, I = ti0 + 1 + c;  // patch-array coordinates
+                if (J < MLAMR_G || J >= pv.NY - MLAMR_G || I < MLAMR_G || I >= pv.NX - MLAMR_G) {
+                    int gi;
+                    if (J < MLAMR_G)
+                        gi = J * pv.NX + I;
+                    else if (J >= pv.NY - MLAMR_G)
+                        gi = 2 * pv.NX + (J - (pv.NY - MLAMR_G)) * pv.NX + I;
+                    else
+                        gi = 4 * pv.NX + (J - MLAMR_G) * 4 + (I < MLAMR_G ? I : I - pv.NX + 4);
+                    const int64_t v = gplan[gbase[p] + gi];
+                    if (v >= 0) ga[i] = src + v;
+                }
+            }
         }
         const int64_t boff = lv.bathy - src;  // same patch layout, one plane
 #pragma unroll
@@ -544,7 +565,7 @@ template <int M>
 static int launch_step(const mlamr_level &lv, const double *src, double *dst,
                        const int32_t *tiles, int n_tiles, double dt, int y_first,
                        const mlamr_params &prm, long long *speed_bits, double *tile_acc,
-                       const int32_t *status, cudaStream_t st) {
+                       const int32_t *status, const int64_t *gbase, const int64_t *gplan, cudaStream_t st) {
     const size_t smem = sizeof(StepSmem<M>);
     static bool configured[2] = {false, false};
     if (!configured[y_first ? 1 : 0]) {
@@ -572,9 +593,11 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
             kc.rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
     kc.coef = (M > 1) ? prm.gravity * (1.0 - kc.rr[0][1]) : 0.0;
     if (y_first)
-        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status);
+        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status,
+                                                   gbase, gplan);
     else
-        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status);
+        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status,
+                                                    gbase, gplan);
     return (int)cudaGetLastError();
 }
 

@@ -145,6 +145,11 @@ class Simulation:
             self._wave_tol = torch.tensor(list(problem.wave_tolerance), dtype=torch.float64, device=self.dev)
         self._flagbuf = {}
         self._scratch_bufs = {}
+        # childless levels: sibling ghost copy inside the step's staging
+        # (mlamr_step with a ghost plan).  Off by default: on C4 it saves the
+        # 0.31 ms copy per finest fill but the plan lookups add ~0.3 ms of
+        # dependent-load latency to each step launch (profiles/r01/README.md)
+        self.fuse_sibling_fill = False
         self.levels: dict[int, LevelPool] = {}
         self.steps = {s.level: 0 for s in self.specs}
         self._stash = {}
@@ -252,7 +257,12 @@ class Simulation:
         return tot.cpu().numpy()
 
     # -- ghost filling (driver.py:157-190) ------------------------------------
-    def fill_level_ghosts(self, level: int, t: float) -> None:
+    def fill_level_ghosts(self, level: int, t: float, siblings: bool = True) -> None:
+        """Ghost frames of a level at time t (driver.py:175-190).  With
+        ``siblings=False`` the sibling copies are left to the step that
+        follows (mlamr_step reads sibling halo cells through the ghost plan);
+        only patches with physical BCs get them, because their BC corners
+        read the copied frame."""
         pool = self.levels[level]
         if pool.P == 0:
             return
@@ -272,6 +282,8 @@ class Simulation:
                 old_ptr = old.data_ptr()
         pl, nl = pool.work_list()
         gbase, plan, cells, n_cells, bc_d, n_bc, max_ghost = pool.ghost_plan()
+        if not siblings:
+            pl, nl = bc_d.data_ptr(), n_bc
         self._call(self.lib.mlamr_fill_ghosts_planned, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
                    self.prm, self.status.data_ptr(), gbase.data_ptr(), plan.data_ptr(), pl, nl, max_ghost,
                    cells.data_ptr(), n_cells, bc_d.data_ptr(), n_bc, self.sh)
@@ -516,7 +528,7 @@ class Simulation:
         self.host_prof["regrid(total)"] += time.perf_counter() - t0
 
     # -- stepping (driver.py:224-309) ------------------------------------------------
-    def _step_patches(self, level: int, dt: float) -> None:
+    def _step_patches(self, level: int, dt: float, fused_siblings: bool = False) -> None:
         pool = self.levels[level]
         if pool.P == 0:
             return
@@ -536,9 +548,13 @@ class Simulation:
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(self.stream)
+        gb = gp = None
+        if fused_siblings:
+            gbase, plan = pool.ghost_plan()[:2]
+            gb, gp = gbase.data_ptr(), plan.data_ptr()
         self._call(self.lib.mlamr_step, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
                    pool.n_tiles, pool.tile_tx, dt, y_first, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
-                   self.status.data_ptr(), self.sh)
+                   self.status.data_ptr(), gb, gp, self.sh)
         if timed:
             e1.record(self.stream)
             self.step_events.append((e0, e1, pool))
@@ -568,11 +584,14 @@ class Simulation:
     def advance_level(self, level: int, dt: float, t0: float) -> None:
         if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:
             self.regrid_from(level)
-        self.fill_level_ghosts(level, t0)
         pool = self.levels[level]
         child = self.levels.get(level + 1)
         has_child = child is not None and child.P > 0
-        self._step_patches(level, dt)
+        # a level without children needs its ghost frames only for its own
+        # step: the sibling part of the fill is fused into the step
+        fuse = self.fuse_sibling_fill and not has_child
+        self.fill_level_ghosts(level, t0, siblings=not fuse)
+        self._step_patches(level, dt, fused_siblings=fuse)
         self.steps[level] += 1
         t1 = t0 + dt
         pool.time = t1

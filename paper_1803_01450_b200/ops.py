@@ -122,7 +122,7 @@ def step_patch(patch, dt: float, params, y_first: bool = False) -> StepResult:
     lv = pool.struct(src)
     N.check(L.mlamr_step(lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(), pool.n_tiles, pool.tile_tx, dt,
                          int(bool(y_first)), prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
-                         status.data_ptr(), sh), "step")
+                         status.data_ptr(), None, None, sh), "step")
     N.check(L.mlamr_step_finalize(lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(), pool.n_tiles,
                                   dt, prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
                                   acc.data_ptr(), status.data_ptr(), bad.data_ptr(), sh), "finalize")

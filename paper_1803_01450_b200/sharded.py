@@ -312,12 +312,13 @@ class ShardedSimulation(Simulation):
         self._refresh(level)                                            # (i)
         if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:
             self.regrid_from(level)
-        self.fill_level_ghosts(level, t0)
-        self._refresh(level)                                            # (ii)
-        pool = self.levels[level]
         child = self.levels.get(level + 1)
         has_child = child is not None and len(self.layout.get(level + 1, _EMPTY)) > 0
-        self._step_patches(level, dt)
+        fuse = self.fuse_sibling_fill and not has_child
+        self.fill_level_ghosts(level, t0, siblings=not fuse)
+        self._refresh(level)                                            # (ii)
+        pool = self.levels[level]
+        self._step_patches(level, dt, fused_siblings=fuse)
         self.steps[level] += 1
         t1 = t0 + dt
         pool.time = t1

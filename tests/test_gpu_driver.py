@@ -103,3 +103,18 @@ def test_config_run_matches_oracle(oracle, name):
     for a, b in ((sg.refine_delta, sc.refine_delta), (sg.derefine_delta, sc.derefine_delta)):
         np.testing.assert_allclose(np.asarray(a, float), np.asarray(b, float), rtol=0, atol=1e-12 * scale)
     np.testing.assert_allclose(gpu.composite_mass(), mass, rtol=1e-12)
+
+
+def test_shelf_small_with_fused_sibling_fill_matches_reference():
+    """The step reading sibling halo cells through the ghost plan (instead
+    of a separate sibling copy) gives the same bits."""
+    from shelf_problem import shelf_problem
+    from paper_1803_01450_b200.driver import Simulation
+    z = load_golden("run_shelf_small.npz")
+    sim = Simulation(shelf_problem())
+    sim.fuse_sibling_fill = True
+    for dtref in z["dts"]:
+        dt = sim.choose_dt()
+        assert dt == float(dtref)
+        sim.advance_coarse_step(dt)
+    _compare_golden(sim, z, "final_")
