@@ -207,6 +207,7 @@ def b200_arm(args):
     sim.step_events = []
     launches0 = N.LAUNCHES[0]
     cells0 = sim.stats.total_cell_updates
+    xbytes0 = getattr(sim, "bytes_exchanged", 0)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -317,6 +318,8 @@ def b200_arm(args):
                                        if world > 1 else "single GPU"),
                        "l2": (f"inputs larger than L2 (device state {pool_bytes / 1e9:.2f} GB)" if pool_bytes > 126e6 else f"device state {pool_bytes / 1e9:.3f} GB fits in L2 (no flush)"),
                        "dt_policy": "reference: level-1 stable_dt, r_t subcycling",
+                       **({"exchange_bytes_per_step_rank0": int((sim.bytes_exchanged - xbytes0) / args.steps)}
+                          if world > 1 else {}),
                        "host_ms_per_step": {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,

@@ -109,11 +109,19 @@ def coarsen_floor(b: np.ndarray, rx: int, ry: int) -> np.ndarray:
 
 
 def needed(level: int, rank: int, layouts: Dict[int, np.ndarray], owners: Dict[int, np.ndarray],
-           ratios: Dict[int, tuple], extra_fine: Optional[Dict[int, np.ndarray]] = None) -> np.ndarray:
+           ratios: Dict[int, tuple], extra_fine: Optional[Dict[int, np.ndarray]] = None,
+           full_only: bool = False, with_children: bool = True) -> np.ndarray:
     """Sorted global indices of level `level` patches rank `rank` must hold
     (owned + shadows).  ratios[l] = (r_x, r_y) between l and l+1.
     ``extra_fine[l+1]`` adds fine boxes (e.g. old layouts during a regrid)
-    whose parent stencils must be present on this level."""
+    whose parent stencils must be present on this level.
+
+    ``full_only``: only the patches that must be held in full -- owned,
+    parents and (``with_children``) children.  The rest are sibling-only
+    shadows: the ghost fill of owned patches reads nothing of them but the
+    interior ring within two cells of their boundary, which is all a
+    refresh sends.  Children are read in full only by the coarsening, so
+    only the refresh in front of it sends them whole."""
     B = layouts.get(level)
     if B is None or len(B) == 0:
         return np.zeros(0, np.int64)
@@ -122,7 +130,8 @@ def needed(level: int, rank: int, layouts: Dict[int, np.ndarray], owners: Dict[i
     need = own.copy()
     mine = B[own]
     # 1. siblings: interiors meeting an owned patch's frame
-    need |= _any_meet(B, grow(mine, G))
+    if not full_only:
+        need |= _any_meet(B, grow(mine, G))
     # 2. parents of owned (and extra) finer patches: full boxes meeting the stencil
     fine = []
     if level + 1 in layouts and len(layouts[level + 1]):
@@ -139,7 +148,7 @@ def needed(level: int, rank: int, layouts: Dict[int, np.ndarray], owners: Dict[i
     # 3. children: finer patches averaged onto owned coarse patches -- the
     # coarse owner needs them; on this level, the patches whose coarse
     # footprint meets an owned patch of level-1
-    if level - 1 in layouts and len(layouts[level - 1]):
+    if (with_children or not full_only) and level - 1 in layouts and len(layouts[level - 1]):
         C = np.asarray(layouts[level - 1], np.int64)
         cown = C[owners[level - 1] == rank]
         rx, ry = ratios[level - 1]
@@ -200,15 +209,21 @@ class Comm:
 @dataclass
 class Transfer:
     """Which patches move between which ranks for one level: for each peer,
-    the (sorted) global indices this rank sends and receives."""
+    the (sorted) global indices this rank sends and receives, and (refresh
+    only) which of them move as the two-cell interior ring only."""
     send: Dict[int, np.ndarray]
     recv: Dict[int, np.ndarray]
+    send_ring: Optional[Dict[int, np.ndarray]] = None
+    recv_ring: Optional[Dict[int, np.ndarray]] = None
 
 
-def plan_refresh(rank: int, world: int, held: Dict[int, np.ndarray], owner: np.ndarray) -> Transfer:
+def plan_refresh(rank: int, world: int, held: Dict[int, np.ndarray], owner: np.ndarray,
+                 full: Optional[Dict[int, np.ndarray]] = None) -> Transfer:
     """Shadow refresh: every rank receives each held foreign patch from its
-    owner; `held[r]` = sorted global indices rank r holds (for all r)."""
-    send, recv = {}, {}
+    owner; `held[r]` = sorted global indices rank r holds (for all r).
+    With `full[r]` (the patches rank r needs in full), the others move as
+    their interior ring only."""
+    send, recv, sring, rring = {}, {}, {}, {}
     mine = held[rank]
     for q in range(world):
         if q == rank:
@@ -216,11 +231,59 @@ def plan_refresh(rank: int, world: int, held: Dict[int, np.ndarray], owner: np.n
         r = mine[owner[mine] == q]
         if len(r):
             recv[q] = r
+            if full is not None:
+                rring[q] = ~np.isin(r, full[rank])
         theirs = held[q]
         s = theirs[owner[theirs] == rank]
         if len(s):
             send[q] = s
-    return Transfer(send, recv)
+            if full is not None:
+                sring[q] = ~np.isin(s, full[q])
+    if full is None:
+        return Transfer(send, recv)
+    return Transfer(send, recv, sring, rring)
+
+
+def ring_segments(boxes: np.ndarray):
+    """Per patch block ((ny+4) x (nx+4), ghost width 2): the two-cell
+    interior ring as (relative offset, length) runs -- the two interior rows
+    next to the bottom and top frame at full block width, then the two
+    interior columns next to the left and right frame on the rows between.
+    Patches too small for a distinct ring are whole blocks.  Returns
+    (patch_index, rel_offset, length, packed_size_per_patch)."""
+    b = np.asarray(boxes, np.int64).reshape(-1, 4)
+    NX = b[:, 2] - b[:, 0] + 1 + 2 * G
+    NY = b[:, 3] - b[:, 1] + 1 + 2 * G
+    pi, ro, ln = [], [], []
+    size = np.zeros(len(b), np.int64)
+    small = (NX - 2 * G <= 4) | (NY - 2 * G <= 4)
+    for k in np.flatnonzero(small):
+        pi.append(np.array([k]))
+        ro.append(np.array([0]))
+        ln.append(np.array([NX[k] * NY[k]]))
+        size[k] = NX[k] * NY[k]
+    big = np.flatnonzero(~small)
+    if len(big):
+        nx_, ny_ = NX[big], NY[big]
+        # the two full-width row runs
+        pi += [big, big]
+        ro += [2 * nx_, (ny_ - 4) * nx_]
+        ln += [2 * nx_, 2 * nx_]
+        # the side pairs on rows 4 .. NY-5
+        nrow = ny_ - 8
+        rep = np.repeat(np.arange(len(big)), nrow)
+        start = np.concatenate([[0], np.cumsum(nrow)[:-1]])
+        J = 4 + np.arange(int(nrow.sum())) - np.repeat(start, nrow)
+        NXr = nx_[rep]
+        pi += [big[rep], big[rep]]
+        ro += [J * NXr + 2, J * NXr + NXr - 4]
+        ln += [np.full(len(J), 2, np.int64), np.full(len(J), 2, np.int64)]
+        size[big] = 4 * nx_ + 4 * nrow
+    pi = np.concatenate(pi) if pi else np.zeros(0, np.int64)
+    ro = np.concatenate(ro) if ro else np.zeros(0, np.int64)
+    ln = np.concatenate(ln) if ln else np.zeros(0, np.int64)
+    order = np.lexsort((ro, pi))
+    return pi[order], ro[order], ln[order], size
 
 
 def plan_acquire(rank: int, world: int, have: Dict[int, np.ndarray], want: Dict[int, np.ndarray],
@@ -249,26 +312,31 @@ def patch_sizes(boxes: np.ndarray) -> np.ndarray:
     return (b[:, 2] - b[:, 0] + 1 + 2 * G) * (b[:, 3] - b[:, 1] + 1 + 2 * G)
 
 
-def run_transfer(comm: Comm, tr: Transfer, sizes: np.ndarray, nplanes: int,
+def run_transfer(comm: Comm, tr: Transfer, sizes: Callable, nplanes: int,
                  src_offsets: Callable[[np.ndarray], np.ndarray],
                  dst_offsets: Callable[[np.ndarray], np.ndarray],
                  pack: Callable, unpack: Callable, dtype, device) -> int:
     """Execute a Transfer: pack owned patch blocks (all planes) per peer,
-    grouped send/recv, unpack into the holder's pool.  `pack(gidx, src_off,
-    buf)` / `unpack(gidx, buf, dst_off)` move whole blocks between a pool
-    and a [nplanes, n] packed buffer.  Returns the bytes sent."""
+    grouped send/recv, unpack into the holder's pool.  `sizes(gidx, ring)`
+    gives the packed elements per patch; `pack(gidx, ring, src_off, buf)` /
+    `unpack(gidx, ring, buf, dst_off)` move whole blocks, or their interior
+    rings where `ring` is set, between a pool and a [nplanes, n] packed
+    buffer.  Returns the bytes sent."""
     sends, recvs = {}, {}
     sent = 0
     for q, g in tr.send.items():
-        n = int(sizes[g].sum())
+        ring = tr.send_ring[q] if tr.send_ring is not None else None
+        n = int(sizes(g, ring).sum())
         buf = torch.empty(nplanes * n, dtype=dtype, device=device)
-        pack(g, src_offsets(g), buf)
+        pack(g, ring, src_offsets(g), buf)
         sends[q] = buf
         sent += buf.numel() * buf.element_size()
     for q, g in tr.recv.items():
-        n = int(sizes[g].sum())
+        ring = tr.recv_ring[q] if tr.recv_ring is not None else None
+        n = int(sizes(g, ring).sum())
         recvs[q] = torch.empty(nplanes * n, dtype=dtype, device=device)
     comm.exchange(sends, recvs)
     for q, g in tr.recv.items():
-        unpack(g, recvs[q], dst_offsets(g))
+        ring = tr.recv_ring[q] if tr.recv_ring is not None else None
+        unpack(g, ring, recvs[q], dst_offsets(g))
     return sent

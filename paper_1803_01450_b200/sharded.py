@@ -33,7 +33,7 @@ import torch.distributed as dist
 from . import _native as N
 from .device import LevelPool, empty_level_struct, paint_child_map
 from .distributed import (Comm, _any_meet, needed, partition, patch_sizes, plan_acquire, plan_refresh,
-                          run_transfer)
+                          ring_segments, run_transfer)
 from .driver import Simulation
 from .mesh import GHOST_WIDTH, IndexBox, boxes_array
 from .regrid import chop_boxes, cluster_boxes
@@ -47,6 +47,12 @@ class ShardedSimulation(Simulation):
         self.comm = comm or Comm()
         self.rank, self.world = self.comm.rank, self.comm.world
         self.layout, self.owner, self.held = {}, {}, {}
+        # per level and rank: the held patches needed in full (owned, parents,
+        # children); the other shadows are refreshed as interior rings
+        self.full = {}
+        self.ring_refresh = True
+        self._ring_cache = {}
+        self._fullc_cache = {}
         self.bytes_exchanged = 0
         self._common_init(problem, device, stream)
         if self.pb.flag_rule[0] == "gradient":
@@ -55,6 +61,7 @@ class ShardedSimulation(Simulation):
         self.layout[1] = b1
         self.owner[1] = np.zeros(1, np.int32)
         self.held[1] = {r: (np.arange(1) if r == 0 else np.zeros(0, np.int64)) for r in range(self.world)}
+        self.full[1] = {r: self.held[1][r].copy() for r in range(self.world)}
         base = self._make_pool(1, b1, self.owner[1], self.held[1][self.rank])
         self._set_initial(base)
         self.levels[1] = base
@@ -75,10 +82,24 @@ class ShardedSimulation(Simulation):
     def _ratios(self):
         return {s.level: (s.r_x, s.r_y) for s in self.specs}
 
-    def _held_all(self, level, layouts, owners, extra=None):
+    def _held_all(self, level, layouts, owners, extra=None, full_only=False, with_children=True):
         R = self._ratios()
-        return {r: needed(level, r, layouts, owners, R, None if extra is None else extra(r))
+        return {r: needed(level, r, layouts, owners, R, None if extra is None else extra(r), full_only=full_only,
+                          with_children=with_children)
                 for r in range(self.world)}
+
+    def _full_all(self, level, layouts, owners, extra=None):
+        """Per rank: the held patches every refresh sends whole (owned and
+        parents); children are sent whole only by the pre-coarsening refresh."""
+        return self._held_all(level, layouts, owners, extra, full_only=True, with_children=False)
+
+    def _full_coarsen(self, level: int):
+        key = (level, id(self.layout.get(level)), id(self.layout.get(level - 1)))
+        ent = self._fullc_cache.get(level)
+        if ent is None or ent[0] != key:
+            ent = (key, self._held_all(level, self.layout, self.owner, full_only=True, with_children=True))
+            self._fullc_cache[level] = ent
+        return ent[1]
 
     def _make_pool(self, level, gboxes, owner, local_g) -> LevelPool:
         local_g = np.asarray(local_g, np.int64)
@@ -91,58 +112,113 @@ class ShardedSimulation(Simulation):
         return pool
 
     # -- shadow transfers --------------------------------------------------------
+    def _ring_table(self, level):
+        """CSR view of ring_segments() for the level's layout (cached)."""
+        lay = self.layout[level]
+        key = (level, id(lay), len(lay))
+        ent = self._ring_cache.get(level)
+        if ent is None or ent[0] != key:
+            rp, ro, ln, rsize = ring_segments(lay)
+            cnt = np.bincount(rp, minlength=len(lay)).astype(np.int64)
+            start = np.concatenate([[0], np.cumsum(cnt)[:-1]]).astype(np.int64)
+            ent = (key, ro, ln, rsize, cnt, start)
+            self._ring_cache[level] = ent
+        return ent[1:]
+
     def _transfer(self, level, tr, src: LevelPool, dst: LevelPool) -> None:
-        sizes = patch_sizes(self.layout[level])
+        full_sz = patch_sizes(self.layout[level])
+        ro, ln, rsize, cnt, start = self._ring_table(level)
         M3 = 3 * self.M
 
-        def pack(g, src_off, buf):
-            sz = sizes[g]
-            n = int(sz.sum())
-            poff = np.concatenate([[0], np.cumsum(sz)[:-1]])
-            src.copy_segments(src.state, src.FS, buf, n, src_off, poff, sz)
+        def nsz(g, ring):
+            if ring is None:
+                return full_sz[g]
+            return np.where(ring, rsize[g], full_sz[g])
 
-        def unpack(g, buf, dst_off):
-            sz = sizes[g]
-            n = int(sz.sum())
-            poff = np.concatenate([[0], np.cumsum(sz)[:-1]])
-            dst.copy_segments(buf, n, dst.state, dst.FS, poff, dst_off, sz)
+        def runs(g, ring, block_off):
+            """(block-relative absolute offsets, packed offsets, lengths) of
+            the runs that move for patches g whose blocks start at block_off."""
+            sz = nsz(g, ring)
+            poff = np.concatenate([[0], np.cumsum(sz)[:-1]]).astype(np.int64)
+            if ring is None or not ring.any():
+                return np.asarray(block_off, np.int64), poff, sz
+            r = np.asarray(ring, bool)
+            k = np.flatnonzero(r)
+            c = cnt[g[k]]
+            idx = np.repeat(start[g[k]], c) + (np.arange(int(c.sum())) - np.repeat(np.cumsum(c) - c, c))
+            r_len = ln[idx]
+            r_abs = np.repeat(np.asarray(block_off, np.int64)[k], c) + ro[idx]
+            # packed offsets: each ring patch's runs are consecutive from its poff
+            cum = np.cumsum(r_len) - r_len
+            first = np.repeat(np.cumsum(c) - c, c)
+            r_pack = np.repeat(poff[k], c) + (cum - cum[first])
+            f = np.flatnonzero(~r)
+            return (np.concatenate([np.asarray(block_off, np.int64)[f], r_abs]),
+                    np.concatenate([poff[f], r_pack]), np.concatenate([full_sz[g[f]], r_len]))
+
+        def pack(g, ring, src_off, buf):
+            a, pk, lens = runs(g, ring, src_off)
+            n = int(nsz(g, ring).sum())
+            src.copy_segments(src.state, src.FS, buf, n, a, pk, lens)
+
+        def unpack(g, ring, buf, dst_off):
+            a, pk, lens = runs(g, ring, dst_off)
+            n = int(nsz(g, ring).sum())
+            dst.copy_segments(buf, n, dst.state, dst.FS, pk, a, lens)
 
         with torch.cuda.stream(self.stream):
             self.bytes_exchanged += run_transfer(
-                self.comm, tr, sizes, M3, lambda g: src.offsets[src.local_of(g)],
+                self.comm, tr, nsz, M3, lambda g: src.offsets[src.local_of(g)],
                 lambda g: dst.offsets[dst.local_of(g)], pack, unpack, torch.float64, self.dev)
 
-    def _refresh(self, level: int) -> None:
+    def _refresh(self, level: int, coarsen: bool = False) -> None:
+        """Shadow refresh; ``coarsen``: the one in front of averaging this
+        level down, which must deliver children whole."""
         if self.world == 1 or level not in self.levels:
             return
-        tr = plan_refresh(self.rank, self.world, self.held[level], self.owner[level])
+        full = None
+        if self.ring_refresh:
+            full = self._full_coarsen(level) if coarsen else self.full.get(level)
+        tr = plan_refresh(self.rank, self.world, self.held[level], self.owner[level], full)
         pool = self.levels[level]
         self._transfer(level, tr, pool, pool)
 
-    def _reshape(self, level: int, new_held) -> None:
+    def _reshape(self, level: int, new_held, new_full=None) -> None:
         """Replace a level's local pool by one holding new_held[rank] (same
-        layout and owners), moving data: local copies + owners' sends."""
+        layout and owners), moving data: local copies + owners' sends.
+        Patches held only as refreshed rings are not complete, so they are
+        fetched whole from their owners rather than copied locally.
+        ``new_full`` = the patches each rank needs in full afterwards
+        (default: all of new_held)."""
+        if new_full is None:
+            new_full = new_held
         old = self.levels[level]
         want = new_held[self.rank]
         # the skip must be a collective decision: a rank whose own set is
         # unchanged may still have to send patches to a rank whose set grew
-        if all(np.array_equal(new_held[r], self.held[level][r]) for r in range(self.world)):
+        old_full = self.full.get(level, self.held[level])
+        if all(np.array_equal(new_held[r], self.held[level][r]) and np.array_equal(new_full[r], old_full[r])
+               for r in range(self.world)):
             self.held[level] = new_held
+            self.full[level] = new_full
             return
+        have = {r: (np.intersect1d(self.held[level][r], old_full[r], assume_unique=True)
+                    if self.ring_refresh else self.held[level][r]) for r in range(self.world)}
         new = self._make_pool(level, self.layout[level], self.owner[level], want)
-        common = np.intersect1d(old.gidx, want, assume_unique=True)
+        common = np.intersect1d(have[self.rank], want, assume_unique=True)
         if len(common):
             sizes = patch_sizes(self.layout[level])[common]
             with torch.cuda.stream(self.stream):
                 new.copy_segments(old.state, old.FS, new.state, new.FS, old.offsets[old.local_of(common)],
                                   new.offsets[new.local_of(common)], sizes)
-        tr = plan_acquire(self.rank, self.world, self.held[level], new_held, self.owner[level])
+        tr = plan_acquire(self.rank, self.world, have, new_held, self.owner[level])
         self._transfer(level, tr, old, new)
         new.time = old.time
         new.ghosts_in_cur = old.ghosts_in_cur
         new.child = old.child
         self.levels[level] = new
         self.held[level] = new_held
+        self.full[level] = new_full
         old.release()
 
     # -- reductions ------------------------------------------------------------------
@@ -250,8 +326,9 @@ class ShardedSimulation(Simulation):
         layouts[level + 1] = nboxes
         owners[level + 1] = new_owner
         # (a) the parent level must hold the stencils of new and old owned fine patches
-        self._reshape(level, self._held_all(level, layouts, owners,
-                                            lambda r: {level + 1: old_layout[old_owner == r]}))
+        ext_fine = lambda r: {level + 1: old_layout[old_owner == r]}  # noqa: E731
+        self._reshape(level, self._held_all(level, layouts, owners, ext_fine),
+                      self._full_all(level, layouts, owners, ext_fine))
         par = self.levels[level]
         # (b) old fine patches overlapping new owned patches
         old = self.levels.get(level + 1)
@@ -264,6 +341,7 @@ class ShardedSimulation(Simulation):
             old = self.levels[level + 1]
         # (c) the new level
         held_new = self._held_all(level + 1, layouts, owners)
+        full_new = self._full_all(level + 1, layouts, owners)
         new = self._make_pool(level + 1, nboxes, new_owner, held_new[self.rank])
         new.time = par.time
         M = self.M
@@ -293,6 +371,7 @@ class ShardedSimulation(Simulation):
         self.layout[level + 1] = nboxes
         self.owner[level + 1] = new_owner
         self.held[level + 1] = held_new
+        self.full[level + 1] = full_new
         self.levels[level + 1] = new
         if old is not None:
             old.release()
@@ -300,7 +379,8 @@ class ShardedSimulation(Simulation):
         self._refresh(level + 1)
         # (e) the level below the new one: its shadow set depends on the new owners
         if level + 2 in self.levels:
-            self._reshape(level + 2, self._held_all(level + 2, layouts, owners))
+            self._reshape(level + 2, self._held_all(level + 2, layouts, owners),
+                          self._full_all(level + 2, layouts, owners))
             fs = self.spec(level + 1)
             new.child = paint_child_map(fs, self.layout[level + 2], fs.r_x, fs.r_y, self.dev, self.stream)
         if not init:
@@ -331,7 +411,7 @@ class ShardedSimulation(Simulation):
             for k in range(s.r_t):
                 self.advance_level(level + 1, dtf, t0 + k * dtf)
             self.levels[level + 1].time = t1
-            self._refresh(level + 1)                                    # (iv)
+            self._refresh(level + 1, coarsen=True)                      # (iv)
             self._average_down(level)
             del self._stash[level]
 

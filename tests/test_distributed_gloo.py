@@ -45,7 +45,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1803_01450_b200.distributed import (Comm, needed, partition, patch_sizes, plan_acquire,
-                                                       plan_refresh, run_transfer)
+                                                       plan_refresh, ring_segments, run_transfer)
         comm = Comm()
         assert comm.world == world and comm.rank == rank
         layouts = _layouts()
@@ -53,46 +53,67 @@ def _worker(rank, world, port, q):
         owners = {1: np.zeros(1, np.int32), 2: partition(layouts[2], 4, 4, world),
                   3: partition(layouts[3], 1, 1, world)}
         held = {lv: {r: needed(lv, r, layouts, owners, ratios) for r in range(world)} for lv in (1, 2, 3)}
+        full = {lv: {r: needed(lv, r, layouts, owners, ratios, full_only=True) for r in range(world)}
+                for lv in (1, 2, 3)}
         M3 = 6
         results = {}
         for lv in (2, 3):
-            B = layouts[lv]
-            sizes = patch_sizes(B)
-            mine = held[lv][rank]
-            offs = np.concatenate([[0], np.cumsum(sizes[mine])[:-1]]).astype(np.int64)
-            FS = int(sizes[mine].sum()) + 1
-            pool = torch.full((M3, FS), -1.0, dtype=torch.float64)
-            for k, g in enumerate(mine):
-                if owners[lv][g] == rank:   # owners know their data: a function of (g, plane, cell)
+            for use_ring in (False, True):
+                B = layouts[lv]
+                sizes = patch_sizes(B)
+                rp, rro, rln, rsize = ring_segments(B)
+                mine = held[lv][rank]
+                offs = np.concatenate([[0], np.cumsum(sizes[mine])[:-1]]).astype(np.int64)
+                FS = int(sizes[mine].sum()) + 1
+                pool = torch.full((M3, FS), -1.0, dtype=torch.float64)
+                for k, g in enumerate(mine):
+                    if owners[lv][g] == rank:   # owners know their data: a function of (g, plane, cell)
+                        vals = g * 1000.0 + torch.arange(M3 * int(sizes[g]), dtype=torch.float64).reshape(M3, -1)
+                        pool[:, offs[k]:offs[k] + sizes[g]] = vals
+                loc = {int(g): int(o) for g, o in zip(mine, offs)}
+
+                def runs(gg, ring):
+                    if not ring:
+                        return [(0, int(sizes[gg]))]
+                    sel = rp == gg
+                    return list(zip(rro[sel].tolist(), rln[sel].tolist()))
+
+                def nsz(g, ring):
+                    r = np.zeros(len(g), bool) if ring is None else ring
+                    return np.where(r, rsize[g], sizes[g])
+
+                def pack(g, ring, src_off, buf):
+                    n = int(nsz(g, ring).sum())
+                    b2 = buf.view(M3, n)
+                    at = 0
+                    for i, (gg, so) in enumerate(zip(g, src_off)):
+                        for (o, ln) in runs(gg, ring is not None and ring[i]):
+                            b2[:, at:at + ln] = pool[:, so + o:so + o + ln]
+                            at += ln
+
+                def unpack(g, ring, buf, dst_off):
+                    n = int(nsz(g, ring).sum())
+                    b2 = buf.view(M3, n)
+                    at = 0
+                    for i, (gg, do) in enumerate(zip(g, dst_off)):
+                        for (o, ln) in runs(gg, ring is not None and ring[i]):
+                            pool[:, do + o:do + o + ln] = b2[:, at:at + ln]
+                            at += ln
+
+                offs_of = lambda g: np.array([loc[int(x)] for x in g], np.int64)
+                tr = plan_refresh(rank, world, held[lv], owners[lv], full[lv] if use_ring else None)
+                run_transfer(comm, tr, nsz, M3, offs_of, offs_of, pack, unpack, torch.float64, "cpu")
+                ok, nring = True, 0
+                for k, g in enumerate(mine):
                     vals = g * 1000.0 + torch.arange(M3 * int(sizes[g]), dtype=torch.float64).reshape(M3, -1)
-                    pool[:, offs[k]:offs[k] + sizes[g]] = vals
-            loc = {int(g): int(o) for g, o in zip(mine, offs)}
-            flat = pool.view(-1)
-
-            def pack(g, src_off, buf):
-                n = int(sizes[g].sum())
-                b2 = buf.view(M3, n)
-                at = 0
-                for gg, so in zip(g, src_off):
-                    b2[:, at:at + sizes[gg]] = pool[:, so:so + sizes[gg]]
-                    at += int(sizes[gg])
-
-            def unpack(g, buf, dst_off):
-                n = int(sizes[g].sum())
-                b2 = buf.view(M3, n)
-                at = 0
-                for gg, do in zip(g, dst_off):
-                    pool[:, do:do + sizes[gg]] = b2[:, at:at + sizes[gg]]
-                    at += int(sizes[gg])
-
-            offs_of = lambda g: np.array([loc[int(x)] for x in g], np.int64)
-            tr = plan_refresh(rank, world, held[lv], owners[lv])
-            run_transfer(comm, tr, sizes, M3, offs_of, offs_of, pack, unpack, torch.float64, "cpu")
-            ok = True
-            for k, g in enumerate(mine):
-                vals = g * 1000.0 + torch.arange(M3 * int(sizes[g]), dtype=torch.float64).reshape(M3, -1)
-                ok &= bool(torch.equal(pool[:, offs[k]:offs[k] + sizes[g]], vals))
-            results[lv] = (ok, len(mine), int((owners[lv][mine] == rank).sum()))
+                    got = pool[:, offs[k]:offs[k] + sizes[g]]
+                    if use_ring and g not in full[lv][rank]:
+                        nring += 1
+                        for (o, ln) in runs(g, True):
+                            ok &= bool(torch.equal(got[:, o:o + ln], vals[:, o:o + ln]))
+                    else:
+                        ok &= bool(torch.equal(got, vals))
+                results[(lv, use_ring)] = (ok, len(mine), int((owners[lv][mine] == rank).sum()), nring)
         # acquire plan symmetry: what rank r receives from s equals what s sends to r
         want = {r: np.union1d(held[3][r], np.arange(min(3, len(layouts[3])))) for r in range(world)}
         tr = plan_acquire(rank, world, held[3], want, owners[3])
@@ -120,14 +141,18 @@ def test_sharded_exchange_world2():
         p.join(timeout=60)
         assert p.exitcode == 0
     shadows = {2: 0, 3: 0}
+    rings = 0
     for r in range(world):
         res, sent, recv, t = out[r]
         assert t == world
-        for lv, (ok, held_n, owned_n) in res.items():
-            assert ok, (r, lv)
+        for (lv, use_ring), (ok, held_n, owned_n, nring) in res.items():
+            assert ok, (r, lv, use_ring)
             assert owned_n > 0, (r, lv)
-            shadows[lv] += held_n - owned_n
+            if not use_ring:
+                shadows[lv] += held_n - owned_n
+            rings += nring
     assert all(v > 0 for v in shadows.values()), shadows   # the exchange had work to do
+    assert rings > 0                                          # sibling-only shadows moved as rings
     # plans are mutually consistent
     for r in range(world):
         for s_ in range(world):
