@@ -160,6 +160,14 @@ int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x, int r_y,
                        mlamr_params prm, double *patch_delta, int blocks_per_patch,
                        const int32_t *status, void *stream);
 
+/* The same coarsening over a flat list of all coarse cells of the fine
+ * level (coarse_base[p] = first coarse cell of fine patch p, prefix sums;
+ * n_coarse in total), without the mass-change partials: the driver's path,
+ * whose blocks stay full for small patches. */
+int mlamr_average_down_flat(mlamr_level fine, mlamr_level coarse, int r_x, int r_y, mlamr_params prm,
+                            const int64_t *coarse_base, int64_t n_coarse, const int32_t *status,
+                            void *stream);
+
 /* ---- K3 + K5: regrid data movement (regrid.py:270-353) -------------------
  * Every new-patch interior cell is copied from the old patch covering it
  * (old.own), else refined from the parent's interiors (gather with
@@ -243,6 +251,19 @@ int mlamr_flags_gradient(mlamr_level lv, const double *state, mlamr_params prm, 
  * [ceil(ny/32)*nx].  Exact integer sums. */
 int mlamr_sat_u8(const uint8_t *map, int ny, int nx, int invert, int32_t *sat, int32_t *scratch,
                  void *stream);
+
+/* Sibling copies as a flat gather/scatter.  mlamr_copy_pairs_of_plan
+ * writes, for every ghost cell of the listed patches (all when NULL), the
+ * pair (destination, source) of element offsets, or (-1, src<0) when the
+ * cell has no sibling source; list_base[k] is the first pair slot of list
+ * entry k (prefix sum of its ghost counts).  mlamr_fill_copy_pairs then
+ * copies the 3M planes for the n_pairs compacted pairs -- the sibling part
+ * of the ghost fill (ghost.py:186-196) with one thread per cell. */
+int mlamr_copy_pairs_of_plan(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
+                             const int32_t *patch_list, int n_list, const int64_t *list_base,
+                             int max_ghost, int64_t *pairs, void *stream);
+int mlamr_fill_copy_pairs(double *state, int64_t field_stride, const int64_t *pairs, int64_t n_pairs,
+                          int num_layers, const int32_t *status, void *stream);
 
 /* Frame records of one level (frames.frame_from_hierarchy + write_frame,
  * frames.py:72-100, 141-163): for each patch p (or each entry of

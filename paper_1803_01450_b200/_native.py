@@ -107,6 +107,11 @@ SIGNATURES = {
                                              c_vp]),
     "mlamr_flags_gradient": (ctypes.c_int, [Level, c_vp, Params, ctypes.c_uint, ctypes.c_double, ctypes.c_int,
                                             c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mlamr_copy_pairs_of_plan": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp,
+                                                c_vp]),
+    "mlamr_fill_copy_pairs": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, ctypes.c_int, c_vp, c_vp]),
+    "mlamr_average_down_flat": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, Params, c_vp,
+                                               ctypes.c_int64, c_vp, c_vp]),
     "mlamr_sat_u8": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_pack_frame": (ctypes.c_int, [Level, c_vp, ctypes.c_int, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
                                         c_vp, c_vp]),

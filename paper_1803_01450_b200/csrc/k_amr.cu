@@ -232,6 +232,45 @@ __global__ void __launch_bounds__(NTA) k_fill_copy(mlamr_level lv, const int64_t
     }
 }
 
+// sibling copies from a flat list of (destination, source) element offsets
+// built from the plan (every ghost cell with a sibling source, owned
+// patches only): a pure gather/scatter over all patches of the level, with
+// no per-patch blocks left idle by small patches (C5's 16x16 patches have
+// 144 ghost cells per 256-thread block in the per-patch kernel).
+template <int M>
+__global__ void __launch_bounds__(NTA) k_fill_copy_pairs(double *__restrict__ state, int64_t FS,
+                                                         const int64_t *__restrict__ pairs, int64_t n,
+                                                         const int32_t *status) {
+    if (status != nullptr && *status != 0) return;
+    for (int64_t c = blockIdx.x * (int64_t)NTA + threadIdx.x; c < n; c += (int64_t)gridDim.x * NTA) {
+        const int64_t dst = pairs[2 * c], src = pairs[2 * c + 1];
+        double v[3 * M];
+#pragma unroll
+        for (int q = 0; q < 3 * M; ++q) v[q] = state[q * FS + src];
+#pragma unroll
+        for (int q = 0; q < 3 * M; ++q) state[q * FS + dst] = v[q];
+    }
+}
+
+// the (destination, source) pairs of a plan: one thread per ghost cell of
+// the listed patches writes its pair, or (-1, -1) when it has no sibling
+__global__ void __launch_bounds__(NTA) k_copy_pairs_of_plan(mlamr_level lv, const int64_t *gbase,
+                                                            const int64_t *plan, const int32_t *plist,
+                                                            const int64_t *pbase, int64_t *pairs) {
+    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+    const PatchView pv = patch_view(lv, p);
+    const int nghost = 4 * pv.NX + 4 * pv.ny;
+    const int64_t out0 = pbase[blockIdx.y];
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nghost; idx += gridDim.x * NTA) {
+        const int64_t src = plan[gbase[p] + idx];
+        int J, I;
+        ghost_cell_of(idx, pv.NX, pv.NY, pv.ny, J, I);
+        const int64_t dst = pv.off + (int64_t)J * pv.NX + I;
+        pairs[2 * (out0 + idx)] = src >= 0 ? dst : -1;
+        pairs[2 * (out0 + idx) + 1] = src;
+    }
+}
+
 // coarse interpolation of the cells of a compacted list (patch, ghost idx)
 template <int M>
 __global__ void __launch_bounds__(NTA) k_fill_interp(mlamr_level lv, mlamr_level par, const double *par_old,
@@ -295,30 +334,19 @@ __global__ void __launch_bounds__(NTA) k_fill_bathy(mlamr_level lv, const double
 // ---------------------------------------------------------------------------
 // RX/RY > 0: compile-time ratios (fully unrolled, all loads in flight);
 // 0: runtime ratios.  Same summation order either way (coarsen.py:21-27).
+// One coarse cell of average_down: block-mean the fine children of coarse
+// cell (clo_i + I, clo_j + J) into the coarse owner's interior (if any) and
+// accumulate the mass change into dsum.
 template <int M, int RX, int RY>
-__global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_level coarse, int r_x_, int r_y_,
-                                                      mlamr_params prm, double *patch_delta,
-                                                      const int32_t *status) {
-    __shared__ double red[NTA];
-    if (status != nullptr && *status != 0) return;
-    const int r_x = RX > 0 ? RX : r_x_;
-    const int r_y = RY > 0 ? RY : r_y_;
-    const int p = blockIdx.y;
-    const PatchView fv = patch_view(fine, p);
-    const int cnx = fv.nx / r_x, cny = fv.ny / r_y;
-    const int clo_i = floordiv(fv.lo_i, r_x), clo_j = floordiv(fv.lo_j, r_y);
+__device__ __forceinline__ void avg_cell(const mlamr_level &fine, const mlamr_level &coarse, const PatchView &fv,
+                                         int r_x, int r_y, int cnx, int clo_i, int clo_j, int idx, double tol,
+                                         double nblk, bool vec2, double (&dsum)[M]) {
     const int64_t FF = fine.field_stride, CF = coarse.field_stride;
-    const double tol = prm.dry_tolerance;
-    const double nblk = (double)(r_x * r_y);
-    const bool vec2 = !((fv.NX | fv.off | FF) & 1);
-    double dsum[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) dsum[m] = 0.0;
-    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
+    do {
         const int J = idx / cnx, I = idx - (idx / cnx) * cnx;
         const int ci = clo_i + I, cj = clo_j + J;
         const int o = owner_at(coarse.own, coarse.level_nx, coarse.level_ny, ci, cj);
-        if (o < 0) continue;
+        if (o < 0) break;
         const int64_t base = fv.off + (int64_t)(MLAMR_G + J * r_y) * fv.NX + (MLAMR_G + I * r_x);
         double avg[3][M];
 #pragma unroll
@@ -378,11 +406,75 @@ __global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_le
             coarse.state[(M + m) * CF + kc] = avg[1][m];
             coarse.state[(2 * M + m) * CF + kc] = avg[2][m];
         }
-    }
+    } while (false);
+}
+
+template <int M, int RX, int RY>
+__global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_level coarse, int r_x_, int r_y_,
+                                                      mlamr_params prm, double *patch_delta,
+                                                      const int32_t *status) {
+    __shared__ double red[NTA];
+    if (status != nullptr && *status != 0) return;
+    const int r_x = RX > 0 ? RX : r_x_;
+    const int r_y = RY > 0 ? RY : r_y_;
+    const int p = blockIdx.y;
+    const PatchView fv = patch_view(fine, p);
+    const int cnx = fv.nx / r_x, cny = fv.ny / r_y;
+    const int clo_i = floordiv(fv.lo_i, r_x), clo_j = floordiv(fv.lo_j, r_y);
+    const double tol = prm.dry_tolerance;
+    const double nblk = (double)(r_x * r_y);
+    const bool vec2 = !((fv.NX | fv.off | fine.field_stride) & 1);
+    double dsum[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) dsum[m] = 0.0;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA)
+        avg_cell<M, RX, RY>(fine, coarse, fv, r_x, r_y, cnx, clo_i, clo_j, idx, tol, nblk, vec2, dsum);
 #pragma unroll
     for (int m = 0; m < M; ++m) {
         const double s = block_sum<NTA>(dsum[m], red);
         if (threadIdx.x == 0) patch_delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
+    }
+}
+
+// average_down over a flat list of all coarse cells of the fine level
+// (cbase[p] = first coarse cell of fine patch p, prefix sums), without the
+// per-patch mass-change partials (the driver does not use them,
+// driver.py:280): small patches (C5's 16x16 fine patches have 32 coarse
+// cells) no longer leave most of a per-patch block idle.
+template <int M, int RX, int RY>
+__global__ void __launch_bounds__(NTA) k_average_down_flat(mlamr_level fine, mlamr_level coarse, int r_x_,
+                                                           int r_y_, mlamr_params prm, const int64_t *cbase,
+                                                           int64_t n_coarse, const int32_t *status) {
+    __shared__ int first_patch;
+    if (status != nullptr && *status != 0) return;
+    const int r_x = RX > 0 ? RX : r_x_;
+    const int r_y = RY > 0 ? RY : r_y_;
+    const double tol = prm.dry_tolerance;
+    const double nblk = (double)(r_x * r_y);
+    double dsum[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) dsum[m] = 0.0;
+    for (int64_t c0 = (int64_t)blockIdx.x * NTA; c0 < n_coarse; c0 += (int64_t)gridDim.x * NTA) {
+        __syncthreads();
+        if (threadIdx.x == 0) {  // patch of the block's first cell: last p with cbase[p] <= c0
+            int lo = 0, hi = fine.num_patches - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (cbase[mid] <= c0) lo = mid; else hi = mid - 1;
+            }
+            first_patch = lo;
+        }
+        __syncthreads();
+        const int64_t c = c0 + threadIdx.x;
+        if (c >= n_coarse) continue;
+        int p = first_patch;
+        while (p + 1 < fine.num_patches && cbase[p + 1] <= c) ++p;
+        const PatchView fv = patch_view(fine, p);
+        const int cnx = fv.nx / r_x;
+        const int clo_i = floordiv(fv.lo_i, r_x), clo_j = floordiv(fv.lo_j, r_y);
+        const bool vec2 = !((fv.NX | fv.off | fine.field_stride) & 1);
+        avg_cell<M, RX, RY>(fine, coarse, fv, r_x, r_y, cnx, clo_i, clo_j, (int)(c - cbase[p]), tol, nblk, vec2,
+                            dsum);
     }
 }
 
@@ -782,6 +874,29 @@ extern "C" int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *pare
     return (int)cudaGetLastError();
 }
 
+extern "C" int mlamr_copy_pairs_of_plan(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
+                                        const int32_t *patch_list, int n_list, const int64_t *list_base,
+                                        int max_ghost, int64_t *pairs, void *stream) {
+    const int nb = patch_list ? n_list : lv.num_patches;
+    if (nb <= 0) return 0;
+    dim3 grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), (unsigned)nb);
+    k_copy_pairs_of_plan<<<grid, NTA, 0, as_stream(stream)>>>(lv, gbase, plan, patch_list, list_base, pairs);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_fill_copy_pairs(double *state, int64_t field_stride, const int64_t *pairs, int64_t n_pairs,
+                                     int num_layers, const int32_t *status, void *stream) {
+    if (n_pairs <= 0) return 0;
+    const int blocks = (int)std::min<int64_t>((n_pairs + NTA - 1) / NTA, 148 * 16);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_fill_copy_pairs<M><<<blocks, NTA, 0, st>>>(state, field_stride, pairs, n_pairs, status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
 extern "C" int mlamr_fill_bathymetry(mlamr_level lv, const double *level_bathy, const int32_t *bcs,
                                      void *stream) {
     if (lv.num_patches <= 0) return 0;
@@ -806,6 +921,27 @@ extern "C" int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x,
             k_average_down<M, 4, 2><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
         else
             k_average_down<M, 0, 0><<<grid, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, patch_delta, status);
+    });
+    if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_average_down_flat(mlamr_level fine, mlamr_level coarse, int r_x, int r_y, mlamr_params prm,
+                                       const int64_t *coarse_base, int64_t n_coarse, const int32_t *status,
+                                       void *stream) {
+    if (fine.num_patches <= 0 || n_coarse <= 0) return 0;
+    const int blocks = (int)std::min<int64_t>((n_coarse + NTA - 1) / NTA, 148 * 16);
+    cudaStream_t st = as_stream(stream);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        if (r_x == 4 && r_y == 4)
+            k_average_down_flat<M, 4, 4><<<blocks, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, coarse_base, n_coarse, status);
+        else if (r_x == 2 && r_y == 2)
+            k_average_down_flat<M, 2, 2><<<blocks, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, coarse_base, n_coarse, status);
+        else if (r_x == 4 && r_y == 2)
+            k_average_down_flat<M, 4, 2><<<blocks, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, coarse_base, n_coarse, status);
+        else
+            k_average_down_flat<M, 0, 0><<<blocks, NTA, 0, st>>>(fine, coarse, r_x, r_y, prm, coarse_base, n_coarse, status);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();

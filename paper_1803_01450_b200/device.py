@@ -348,6 +348,51 @@ class LevelPool:
         self._plan = (gbase_d, plan, cells, int(cells.shape[0]), bc_d, len(bcp), int(ng.max()) if len(ng) else 0)
         return self._plan
 
+    def coarse_base(self, rx: int, ry: int):
+        """(device int64 prefix sums of the coarse cells under each patch,
+        total) for the flat average_down.  All local patches: under
+        sharding the coarse owner averages the children it holds as
+        shadows (delivered whole by the pre-coarsening refresh)."""
+        key = (rx, ry)
+        cache = getattr(self, "_cbase", None)
+        if cache is None or cache[0] != key:
+            b = self.boxes
+            n = ((b[:, 2] - b[:, 0] + 1) // rx) * ((b[:, 3] - b[:, 1] + 1) // ry) if self.P else np.zeros(0, np.int64)
+            base = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+            with torch.cuda.stream(self.stream):
+                d = arena().upload(base, self.device, self.stream)
+            cache = (key, d, int(base[-1]))
+            self._cbase = cache
+        return cache[1], cache[2]
+
+    def copy_pairs(self):
+        """(device int64 [n, 2] (destination, source) offsets, n): the sibling
+        copies of the ghost fill for the owned patches (built once per layout)."""
+        if getattr(self, "_pairs", None) is not None:
+            return self._pairs
+        gbase_d, plan = self.ghost_plan()[:2]
+        b = self.boxes
+        ng = 4 * (b[:, 2] - b[:, 0] + 1 + 2 * GHOST_WIDTH) + 4 * (b[:, 3] - b[:, 1] + 1)
+        A = arena()
+        lst = np.flatnonzero(self.owned) if self.owned is not None else np.arange(self.P)
+        if len(lst):
+            lbase = np.concatenate([[0], np.cumsum(ng[lst])[:-1]]).astype(np.int64)
+            ltot = int(ng[lst].sum())
+            with torch.cuda.stream(self.stream):
+                pl_d = A.upload(lst.astype(np.int32), self.device, self.stream)
+                lb_d = A.upload(lbase, self.device, self.stream)
+                raw = torch.empty(2 * ltot, dtype=torch.int64, device=self.device)
+                N.check(N.lib().mlamr_copy_pairs_of_plan(self.struct(), gbase_d.data_ptr(), plan.data_ptr(),
+                                                         pl_d.data_ptr(), len(lst), lb_d.data_ptr(),
+                                                         int(ng.max()), raw.data_ptr(), self.stream.cuda_stream),
+                        "copy_pairs_of_plan")
+                raw = raw.view(-1, 2)
+                pairs = raw[raw[:, 0] >= 0].contiguous()
+            self._pairs = (pairs, int(pairs.shape[0]))
+        else:
+            self._pairs = (torch.zeros(2, dtype=torch.int64, device=self.device), 0)
+        return self._pairs
+
     def work_list(self):
         """(device patch-list pointer, count) of the patches this rank owns,
         or (None, 0) when it owns them all (single-GPU runs)."""

@@ -280,9 +280,19 @@ class Simulation:
                 t0, dt, old = st
                 theta = min(1.0, max(0.0, (t - t0) / dt)) if dt > 0 else 1.0
                 old_ptr = old.data_ptr()
-        pl, nl = pool.work_list()
         gbase, plan, cells, n_cells, bc_d, n_bc, max_ghost = pool.ghost_plan()
-        if not siblings:
+        if siblings and max_ghost < 256:
+            # small patches (fewer ghost cells than a block has threads):
+            # the sibling copies as one flat gather/scatter, before the
+            # planned fill (whose BC pass reads copied corner cells), which
+            # then skips them
+            pairs, n_pairs = pool.copy_pairs()
+            self._call(self.lib.mlamr_fill_copy_pairs, pool.state.data_ptr(), pool.FS, pairs.data_ptr(), n_pairs,
+                       self.M, self.status.data_ptr(), self.sh)
+            pl, nl = bc_d.data_ptr(), 0
+        elif siblings:
+            pl, nl = pool.work_list()
+        else:
             pl, nl = bc_d.data_ptr(), n_bc
         self._call(self.lib.mlamr_fill_ghosts_planned, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
                    self.prm, self.status.data_ptr(), gbase.data_ptr(), plan.data_ptr(), pl, nl, max_ghost,
@@ -574,12 +584,9 @@ class Simulation:
         if abs(fine.time - coarse.time) > _TIME_RTOL * max(1.0, abs(coarse.time)):
             raise TimeSyncError(f"level {level + 1} at t={fine.time!r} vs level {level} at t={coarse.time!r}")
         s = self.spec(level)
-        bpp = fine.blocks_per_patch(fine.max_interior // (s.r_x * s.r_y))
-        with torch.cuda.stream(self.stream):
-            part = self._scratch("coarsen", fine.P * bpp * self.M, zero=False)
-        self._call(self.lib.mlamr_average_down, fine.struct(), coarse.struct(), s.r_x, s.r_y, self.prm,
-                   part.data_ptr(), bpp, self.status.data_ptr(), self.sh)
-        self._part_keep = part
+        cbase, n_coarse = fine.coarse_base(s.r_x, s.r_y)
+        self._call(self.lib.mlamr_average_down_flat, fine.struct(), coarse.struct(), s.r_x, s.r_y, self.prm,
+                   cbase.data_ptr(), n_coarse, self.status.data_ptr(), self.sh)
 
     def advance_level(self, level: int, dt: float, t0: float) -> None:
         if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:
