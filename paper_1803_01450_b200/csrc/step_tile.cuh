@@ -567,8 +567,13 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
                        const mlamr_params &prm, long long *speed_bits, double *tile_acc,
                        const int32_t *status, const int64_t *gbase, const int64_t *gplan, cudaStream_t st) {
     const size_t smem = sizeof(StepSmem<M>);
-    static bool configured[2] = {false, false};
-    if (!configured[y_first ? 1 : 0]) {
+    // the shared-memory opt-in is a per-device function attribute
+    constexpr int kMaxDev = 64;
+    static bool configured[kMaxDev][2] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) return -4;
+    if (!configured[dev][y_first ? 1 : 0]) {
         cudaError_t e;
         if (y_first)
             e = cudaFuncSetAttribute(k_step<M, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -582,7 +587,7 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
             e = cudaFuncSetAttribute(k_step<M, false>, cudaFuncAttributePreferredSharedMemoryCarveout, MLAMR_STEP_CARVEOUT);
         if (e != cudaSuccess) return (int)e;
 #endif
-        configured[y_first ? 1 : 0] = true;
+        configured[dev][y_first ? 1 : 0] = true;
     }
     if (n_tiles <= 0) return 0;
     StepConst kc;
