@@ -61,6 +61,47 @@ typedef struct mlamr_level {
     const int32_t *gown;          /* frame-owner map (first wins) or NULL */
 } mlamr_level;
 
+/* ---- patch table: the handle-based runtime -------------
+ * A stateful level/patch manager over the kernels below, for callers that
+ * hold the reference's host Patch arrays (mesh.py:158-232): every argument
+ * is a HOST pointer or a size.  Per patch, h/hu/hv are (M, ny+4, nx+4) and
+ * bathy (ny+4, nx+4) row-major float64 arrays, ghost frames included.
+ * Return values: 0, a CUDA error code, -1 (bad handle/level), -2 (out of
+ * memory), or MLAMR_ST_* status bits (CFL violation: nothing was written,
+ * as physics.py:342-347 raises before touching a patch).
+ *   create / destroy / set_level(level, nx, ny, dx, dy, r_x, r_y, r_t of
+ *   the ratio to level+1) / set_level_bathymetry(in-domain [ny][nx], used
+ *   by regrid for new patches) / upload_patches (replaces the level's
+ *   patches) / download (current state incl. frames) / num_patches /
+ *   max_speed (stable_dt's speeds, physics.py:261-289) / stash(t0, dt)
+ *   (the current state becomes the time-blend source of the children,
+ *   driver.py:260-264) / fill_ghosts(t) (driver.py:175-190) / step_level
+ *   (out_counters[M+2] = clipped depth sums per layer, shear fixes,
+ *   wet-prefix repairs) / average_down(fine level) / regrid(level, new
+ *   boxes) (regrid.rebuild_child_level's data movement, refine and
+ *   derefine mass deltas [M]) / composite_mass(out[M]) / check_finite. */
+typedef struct mlamr_pt mlamr_pt;
+mlamr_pt *mlamr_pt_create(mlamr_params prm, const int32_t *h_bcs, void *stream);
+void mlamr_pt_destroy(mlamr_pt *pt);
+int mlamr_pt_set_level(mlamr_pt *pt, int level, int nx, int ny, double dx, double dy, int r_x, int r_y, int r_t);
+int mlamr_pt_set_level_bathymetry(mlamr_pt *pt, int level, const double *h_bathy);
+int mlamr_pt_upload_patches(mlamr_pt *pt, int level, int n, const int32_t *h_boxes, const double *const *h,
+                            const double *const *hu, const double *const *hv, const double *const *h_bathy);
+int mlamr_pt_download(mlamr_pt *pt, int level, double *const *h, double *const *hu, double *const *hv);
+int mlamr_pt_num_patches(mlamr_pt *pt, int level);
+int mlamr_pt_max_speed(mlamr_pt *pt, int level, double *h_out_speed);
+int mlamr_pt_stash(mlamr_pt *pt, int level, double t0, double dt);
+int mlamr_pt_clear_stash(mlamr_pt *pt, int level);
+int mlamr_pt_fill_ghosts(mlamr_pt *pt, int level, double t);
+int mlamr_pt_step_level(mlamr_pt *pt, int level, double dt, int y_first, double *h_out_counters,
+                        int *h_bad_patch);
+int mlamr_pt_average_down(mlamr_pt *pt, int fine_level);
+int mlamr_pt_regrid(mlamr_pt *pt, int level, int n, const int32_t *h_new_boxes, double *h_out_refine,
+                    double *h_out_derefine);
+int mlamr_pt_composite_mass(mlamr_pt *pt, double *h_out);
+int mlamr_pt_check_finite(mlamr_pt *pt);
+int mlamr_pt_status(mlamr_pt *pt);
+
 /* ---- library ------------------------------------------------------------ */
 /* Number of exported entry points / a version string (for smoke checks). */
 int mlamr_version(void);

@@ -112,6 +112,24 @@ SIGNATURES = {
     "mlamr_fill_copy_pairs": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, ctypes.c_int, c_vp, c_vp]),
     "mlamr_average_down_flat": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, Params, c_vp,
                                                ctypes.c_int64, c_vp, c_vp]),
+    "mlamr_pt_create": (ctypes.c_void_p, [Params, c_vp, c_vp]),
+    "mlamr_pt_destroy": (None, [c_vp]),
+    "mlamr_pt_set_level": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                          ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "mlamr_pt_set_level_bathymetry": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
+    "mlamr_pt_upload_patches": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "mlamr_pt_download": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
+    "mlamr_pt_num_patches": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "mlamr_pt_max_speed": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp]),
+    "mlamr_pt_stash": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_double]),
+    "mlamr_pt_clear_stash": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "mlamr_pt_fill_ghosts": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_double]),
+    "mlamr_pt_step_level": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_double, ctypes.c_int, c_vp, c_vp]),
+    "mlamr_pt_average_down": (ctypes.c_int, [c_vp, ctypes.c_int]),
+    "mlamr_pt_regrid": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp]),
+    "mlamr_pt_composite_mass": (ctypes.c_int, [c_vp, c_vp]),
+    "mlamr_pt_check_finite": (ctypes.c_int, [c_vp]),
+    "mlamr_pt_status": (ctypes.c_int, [c_vp]),
     "mlamr_sat_u8": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_pack_frame": (ctypes.c_int, [Level, c_vp, ctypes.c_int, c_vp, c_vp, ctypes.c_int, ctypes.c_int,
                                         c_vp, c_vp]),

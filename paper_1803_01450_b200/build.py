@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
 OUT = os.path.join(OUT_DIR, "libmlamr_b200.so")
-SOURCES = ["k_step.cu", "k_amr.cu", "host_cluster.cpp"]
+SOURCES = ["k_step.cu", "k_amr.cu", "patch_table.cu", "host_cluster.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-fmad=false", "-Xcompiler", "-fPIC,-O2,-fopenmp",
          "-lgomp", "-shared", "-I" + os.path.join(os.path.dirname(HERE), "include")]
