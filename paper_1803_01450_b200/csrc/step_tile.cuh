@@ -87,7 +87,7 @@ __device__ __forceinline__ bool rect_all_wet(const StepSmem<M> &s, int r0, int r
 // (C * (h0^2 - h0^2) with finite h0), and the wet/co-wet selects go.  The
 // arithmetic that remains is operation for operation the general path's.
 template <int M, int DIR, bool FIRST, bool AW>
-__device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
+__device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
                            const mlamr_params &prm, const double (&rr)[4][4], double &best) {
     // lam = dt / d and yd = recip_nr(d) come from the kernel prologue, where
     // their latency overlaps the tile's in-flight loads
@@ -269,7 +269,11 @@ __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     })
     __syncthreads();
 
-    // ---- Phase C: conservative update + pressure correction + source
+    // ---- Phase C: conservative update + pressure correction + source.
+    // The updated cells are exactly the cells the other sweep reads, so
+    // their wetness decides (block-wide, with the closing barrier) whether
+    // that sweep can take the all-wet path.
+    bool wet_out = true;
     FOR_RECT(ur0, ur1, uc0, uc1, {
         const int k = r * PX + c;
         const int km = k - STEP, kp = k + STEP;
@@ -286,7 +290,9 @@ __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             // upwinded transverse flux (physics.py:155-161)
             const double fvl = fhl > 0.0 ? fhl * s.v[m][km] : (fhl < 0.0 ? fhl * s.v[m][k] : 0.0);
             const double fvr = fhr > 0.0 ? fhr * s.v[m][k] : (fhr < 0.0 ? fhr * s.v[m][kp] : 0.0);
-            H[k] = h0 - lam * (fhr - fhl);
+            const double hnew = h0 - lam * (fhr - fhl);
+            H[k] = hnew;
+            wet_out = wet_out & (hnew > tol) & (hnew < 1e150);
             double hn;
             if (AW && m < M - 1) {
                 // both faces reconstruct to h0: the correction is exactly +0
@@ -325,7 +331,7 @@ __device__ void sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             HT[k] = HT[k] - lam * (fvr - fvl);
         }
     })
-    __syncthreads();
+    return __syncthreads_and(wet_out) != 0;
 }
 
 template <int M, bool YFIRST>
@@ -411,15 +417,14 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     // every layer (~90 % of C4's level-3 tiles)
     const double wtol = prm.dry_tolerance;
     const bool aw1 = rect_all_wet<M>(s, 0, ny2, 0, nx2, wtol);
+    bool aw2;
     if (YFIRST) {
-        if (aw1) sweep_tile<M, 1, true, true>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
-        else sweep_tile<M, 1, true, false>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
+        if (aw1) aw2 = sweep_tile<M, 1, true, true>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
+        else aw2 = sweep_tile<M, 1, true, false>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
     } else {
-        if (aw1) sweep_tile<M, 0, true, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
-        else sweep_tile<M, 0, true, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
+        if (aw1) aw2 = sweep_tile<M, 0, true, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
+        else aw2 = sweep_tile<M, 0, true, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
     }
-    const bool aw2 = YFIRST ? rect_all_wet<M>(s, 1, ny2 - 1, 0, nx2, wtol)
-                            : rect_all_wet<M>(s, 0, ny2, 1, nx2 - 1, wtol);
     if (YFIRST) {
         if (aw2) sweep_tile<M, 0, false, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
         else sweep_tile<M, 0, false, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
