@@ -64,29 +64,18 @@ __device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
 //   C  per cell:      conservative update + pressure correction + source
 // DIR 0 = x (interfaces between columns c, c+1), 1 = y (rows r, r+1).
 // FIRST: all halo lines (the reference's full=True); else interior lines.
-// Is every cell of the rectangle wet in every layer (tol < h < 1e150)?
-// Block-wide; such a sweep takes the AW path of sweep_tile.
-template <int M>
-__device__ __forceinline__ bool rect_all_wet(const StepSmem<M> &s, int r0, int r1, int c0, int c1, double tol) {
-    bool ok = true;
-    FOR_RECT(r0, r1, c0, c1, {
-        const int k = r * PX + c;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            const double h = s.S[m][k];
-            ok = ok & (h > tol) & (h < 1e150);
-        }
-    })
-    return __syncthreads_and(ok) != 0;
-}
-
-// AW: every cell the sweep reads is wet in every layer (rect_all_wet), so
+// AW: every cell the sweep reads is wet in every layer (tol < h < 1e150), so
 // every pair is co-wet and the predicates below are known: the upper
 // layers' reconstruction is the identity (Zl = Zr = 0 and h > 0 give
 // (h + 0) - 0 = h exactly), their pressure correction is exactly +0
 // (C * (h0^2 - h0^2) with finite h0), and the wet/co-wet selects go.  The
 // arithmetic that remains is operation for operation the general path's.
-template <int M, int DIR, bool FIRST, bool AW>
+//
+// One call runs phase A (RUN_A, all-wet path AWA) and/or phases B-C
+// (RUN_BC, all-wet path AW) and returns, block-wide, whether every cell
+// phase A read (RUN_A only) or every cell phase C updated is wet in every
+// layer -- the all-wet decision for what follows.
+template <int M, int DIR, bool FIRST, bool AWA, bool AW, bool RUN_A, bool RUN_BC>
 __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
                            const mlamr_params &prm, const double (&rr)[4][4], double &best) {
     // lam = dt / d and yd = recip_nr(d) come from the kernel prologue, where
@@ -106,63 +95,68 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     const int fr1 = DIR == 1 ? ny2 - 1 : lr1;
     const int fc1 = DIR == 0 ? nx2 - 1 : lc1;
 
-    // ---- Phase A: per-cell inputs on the pre-sweep state of this direction
-    FOR_RECT(lr0, lr1, lc0, lc1, {
-        const int k = r * PX + c;
-        double h[M];
-        double hs = 0.0;
-        bool w = true;
+    if (RUN_A) {
+        bool wet_in = true;
+        // ---- Phase A: per-cell inputs on the pre-sweep state of this direction
+        FOR_RECT(lr0, lr1, lc0, lc1, {
+            const int k = r * PX + c;
+            double h[M];
+            double hs = 0.0;
+            bool w = true;
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-            h[m] = s.S[m][k];
-            hs = hs + h[m];
-            w = w && (h[m] > tol);
-        }
-        // AW: hs > tol > 0, so numpy's maximum(hs, 0) is hs
-        const double cw = sqrt(g * (AW ? hs : np_max(hs, 0.0)));
-        s.cw[k] = cw;
-        if (!AW) s.cowet[k] = (M == 1) ? 1 : w;
-        if (M > 1) {
-            double e = B[k];
-#pragma unroll
-            for (int m = M - 1; m >= 1; --m) {
-                e = e + h[m];
-                s.eb[m - 1][k] = e;
+            for (int m = 0; m < M; ++m) {
+                h[m] = s.S[m][k];
+                hs = hs + h[m];
+                w = w && (h[m] > tol);
+                wet_in = wet_in & (h[m] > tol) & (h[m] < 1e150);
             }
-        }
-        const bool interior = FIRST && r >= 1 && r < ny2 - 1 && c >= 1 && c < nx2 - 1 && (AW || hs > tol);
-        if (FIRST) s.wetcol[k] = hs > tol;
+            // AW: hs > tol > 0, so numpy's maximum(hs, 0) is hs
+            const double cw = sqrt(g * (AWA ? hs : np_max(hs, 0.0)));
+            s.cw[k] = cw;
+            if (!AWA) s.cowet[k] = (M == 1) ? 1 : w;
+            if (M > 1) {
+                double e = B[k];
 #pragma unroll
-        for (int m = 0; m < M; ++m) {
-            const bool wet = AW || h[m] > tol;
-            const double hn = s.S[(DIR == 0 ? M : 2 * M) + m][k];
-            const double ht = s.S[(DIR == 0 ? 2 * M : M) + m][k];
-            double u = 0.0, v = 0.0;
-            if (wet) {
-                bool ok = true;
-                const double y = recip_nr(h[m]);
-                u = div_fast(hn, h[m], y, ok);
-                v = div_fast(ht, h[m], y, ok);
-                if (!ok) {
-                    u = hn / h[m];
-                    v = ht / h[m];
+                for (int m = M - 1; m >= 1; --m) {
+                    e = e + h[m];
+                    s.eb[m - 1][k] = e;
                 }
             }
-            s.u[m][k] = u;
-            s.v[m][k] = v;
-            if (interior) {
-                // observed_max_speed (physics.py:261-278): speed = max(0, x_0,
-                // .., x_{M-1}) + cw with x_m = wet ? max(|hu|/h, |hv|/h) : 0 and
-                // |hu|/h == |hu/h|.  Rounding is monotone, so
-                // max_m(x_m) + cw == max_m(x_m + cw) and 0 + cw == cw: the
-                // running max below is bit-identical to the reference's.
-                const double x = wet ? np_max(fabs(u), fabs(v)) : 0.0;
-                const double cand = (m == 0) ? np_max(cw, x + cw) : x + cw;
-                best = (best < 0.0) ? cand : np_max(best, cand);
+            const bool interior = FIRST && r >= 1 && r < ny2 - 1 && c >= 1 && c < nx2 - 1 && (AWA || hs > tol);
+            if (FIRST) s.wetcol[k] = hs > tol;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const bool wet = AWA || h[m] > tol;
+                const double hn = s.S[(DIR == 0 ? M : 2 * M) + m][k];
+                const double ht = s.S[(DIR == 0 ? 2 * M : M) + m][k];
+                double u = 0.0, v = 0.0;
+                if (wet) {
+                    bool ok = true;
+                    const double y = recip_nr(h[m]);
+                    u = div_fast(hn, h[m], y, ok);
+                    v = div_fast(ht, h[m], y, ok);
+                    if (!ok) {
+                        u = hn / h[m];
+                        v = ht / h[m];
+                    }
+                }
+                s.u[m][k] = u;
+                s.v[m][k] = v;
+                if (interior) {
+                    // observed_max_speed (physics.py:261-278): speed = max(0, x_0,
+                    // .., x_{M-1}) + cw with x_m = wet ? max(|hu|/h, |hv|/h) : 0 and
+                    // |hu|/h == |hu/h|.  Rounding is monotone, so
+                    // max_m(x_m) + cw == max_m(x_m + cw) and 0 + cw == cw: the
+                    // running max below is bit-identical to the reference's.
+                    const double x = wet ? np_max(fabs(u), fabs(v)) : 0.0;
+                    const double cand = (m == 0) ? np_max(cw, x + cw) : x + cw;
+                    best = (best < 0.0) ? cand : np_max(best, cand);
+                }
             }
-        }
-    })
-    __syncthreads();
+        })
+        const bool all_in = __syncthreads_and(wet_in) != 0;
+        if (!RUN_BC) return all_in;
+    }
 
     // ---- Phase B: HLL fluxes per interface (physics.py:101-161) + sources
     FOR_RECT(lr0, fr1, lc0, fc1, {
@@ -331,8 +325,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             HT[k] = HT[k] - lam * (fvr - fvl);
         }
     })
-    return __syncthreads_and(wet_out) != 0;
-}
+    return __syncthreads_and(wet_out) != 0;}
+
 
 template <int M, bool YFIRST>
 __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, const double *__restrict__ src,
@@ -415,23 +409,20 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     double best = -1.0;  // running observed speed over this thread's cells
     // each sweep takes the all-wet path when every cell it reads is wet in
     // every layer (~90 % of C4's level-3 tiles)
-    const double wtol = prm.dry_tolerance;
-    const bool aw1 = rect_all_wet<M>(s, 0, ny2, 0, nx2, wtol);
-    bool aw2;
-    if (YFIRST) {
-        if (aw1) aw2 = sweep_tile<M, 1, true, true>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
-        else aw2 = sweep_tile<M, 1, true, false>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
-    } else {
-        if (aw1) aw2 = sweep_tile<M, 0, true, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
-        else aw2 = sweep_tile<M, 0, true, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
-    }
-    if (YFIRST) {
-        if (aw2) sweep_tile<M, 0, false, true>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
-        else sweep_tile<M, 0, false, false>(s, ny2, nx2, dt, lv.dx, lam_x, y_x, prm, rr, best);
-    } else {
-        if (aw2) sweep_tile<M, 1, false, true>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
-        else sweep_tile<M, 1, false, false>(s, ny2, nx2, dt, lv.dy, lam_y, y_y, prm, rr, best);
-    }
+    // phase A of the first sweep runs the general path and finds out
+    // whether the rest of that sweep can take the all-wet path; the
+    // first sweep's update does the same for the second sweep
+    constexpr int D1 = YFIRST ? 1 : 0, D2 = YFIRST ? 0 : 1;
+    const double d1 = YFIRST ? lv.dy : lv.dx, d2 = YFIRST ? lv.dx : lv.dy;
+    const double l1 = YFIRST ? lam_y : lam_x, l2 = YFIRST ? lam_x : lam_y;
+    const double q1 = YFIRST ? y_y : y_x, q2 = YFIRST ? y_x : y_y;
+    const bool aw1 = sweep_tile<M, D1, true, false, false, true, false>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best);
+    const bool aw2 = aw1 ? sweep_tile<M, D1, true, false, true, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best)
+                         : sweep_tile<M, D1, true, false, false, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best);
+    if (aw2)
+        sweep_tile<M, D2, false, true, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best);
+    else
+        sweep_tile<M, D2, false, false, false, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best);
 
     // post-processing on the tile interior (physics.py:360-376)
     const double tol = prm.dry_tolerance;
