@@ -57,6 +57,85 @@ __device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
     return (m == M - 1) ? s.S[3 * M][k] : s.eb[m < M - 1 ? m : 0][k];
 }
 
+// Post-processing of one interior cell (physics.py:360-376): clip negative
+// depths, the shear blend (M = 2), the wet-prefix repair and zeroing dry
+// momenta, then the store to the destination state.  Runs inside the last
+// sweep's update, on the values that update produced.
+struct PostCtx {
+    double *dst;
+    int64_t base, FS;
+    int NX;
+    double tol, coef;
+    double negs[MLAMR_MAX_LAYERS];
+    long long fixes, repairs;
+};
+
+template <int M>
+__device__ __forceinline__ void post_cell(double (&h)[M], double (&hu)[M], double (&hv)[M], PostCtx &pc, int r,
+                                          int c) {
+    const double tol = pc.tol, coef = pc.coef;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        const double neg = np_min(h[m], 0.0);
+        pc.negs[m] = pc.negs[m] + neg;
+        if (neg < 0.0) h[m] = 0.0;
+    }
+    if (M == 2) {  // _blend_shear (physics.py:292-327)
+        const double h1 = h[0], h2 = h[1 % M];
+        if (h1 > tol && h2 > tol) {
+            const double hu1 = hu[0], hu2 = hu[1 % M], hv1 = hv[0], hv2 = hv[1 % M];
+            bool ok = true;
+            const double y1 = recip_nr(h1), y2 = recip_nr(h2);
+            double u1 = div_fast(hu1, h1, y1, ok), v1 = div_fast(hv1, h1, y1, ok);
+            double u2 = div_fast(hu2, h2, y2, ok), v2 = div_fast(hv2, h2, y2, ok);
+            if (!ok) {
+                u1 = hu1 / h1;
+                u2 = hu2 / h2;
+                v1 = hv1 / h1;
+                v2 = hv2 / h2;
+            }
+            const double du = u1 - u2, dv = v1 - v2;
+            const double shear2 = (du * du) + (dv * dv);
+            const double bound = coef * (h1 + h2);
+            if (shear2 > bound) {
+                ++pc.fixes;
+                const double alpha = sqrt(bound / shear2);
+                const double htot = h1 + h2;
+                const double umean = (hu1 + hu2) / htot;
+                const double vmean = (hv1 + hv2) / htot;
+                hu[0] = h1 * (umean + alpha * (u1 - umean));
+                hu[1 % M] = h2 * (umean + alpha * (u2 - umean));
+                hv[0] = h1 * (vmean + alpha * (v1 - vmean));
+                hv[1 % M] = h2 * (vmean + alpha * (v2 - vmean));
+            }
+        }
+    }
+    // restore_wet_prefix (state.py:125-145), then zero_dry_momenta (:104-110)
+#pragma unroll
+    for (int m = 1; m < M; ++m) {
+        if (h[m] > tol && h[m - 1] <= tol) {
+            ++pc.repairs;
+            h[m - 1] = h[m - 1] + h[m];
+            hu[m - 1] = hu[m - 1] + hu[m];
+            hv[m - 1] = hv[m - 1] + hv[m];
+            h[m] = 0.0;
+            hu[m] = 0.0;
+            hv[m] = 0.0;
+        }
+    }
+    const int64_t gaddr = pc.base + (int64_t)r * pc.NX + c;
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        if (h[m] <= tol) {
+            hu[m] = 0.0;
+            hv[m] = 0.0;
+        }
+        pc.dst[m * pc.FS + gaddr] = h[m];
+        pc.dst[(M + m) * pc.FS + gaddr] = hu[m];
+        pc.dst[(2 * M + m) * pc.FS + gaddr] = hv[m];
+    }
+}
+
 // One directional sweep of all layers over the staged tile
 // (physics._sweep_x / _sweep_y with _layer_inputs), three phases:
 //   A  per cell:      layer inputs (cw, cowet, eta_{m+1}) and velocities
@@ -75,9 +154,10 @@ __device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
 // (RUN_BC, all-wet path AW) and returns, block-wide, whether every cell
 // phase A read (RUN_A only) or every cell phase C updated is wet in every
 // layer -- the all-wet decision for what follows.
-template <int M, int DIR, bool FIRST, bool AWA, bool AW, bool RUN_A, bool RUN_BC>
+template <int M, int DIR, bool FIRST, bool AWA, bool AW, bool RUN_A, bool RUN_BC, bool LAST = false>
 __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
-                           const mlamr_params &prm, const double (&rr)[4][4], double &best) {
+                           const mlamr_params &prm, const double (&rr)[4][4], double &best,
+                           PostCtx *post = nullptr) {
     // lam = dt / d and yd = recip_nr(d) come from the kernel prologue, where
     // their latency overlaps the tile's in-flight loads
     const double g = prm.gravity;
@@ -273,6 +353,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
         const int km = k - STEP, kp = k + STEP;
         const bool copl = AW || (s.cowet[km] && s.cowet[k]);
         const bool copr = AW || (s.cowet[k] && s.cowet[kp]);
+        double nh[M], nn[M], nt[M];   // LAST: the updated cell stays in registers
 #pragma unroll
         for (int m = 0; m < M; ++m) {
             double *H = s.S[m];
@@ -285,7 +366,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             const double fvl = fhl > 0.0 ? fhl * s.v[m][km] : (fhl < 0.0 ? fhl * s.v[m][k] : 0.0);
             const double fvr = fhr > 0.0 ? fhr * s.v[m][k] : (fhr < 0.0 ? fhr * s.v[m][kp] : 0.0);
             const double hnew = h0 - lam * (fhr - fhl);
-            H[k] = hnew;
+            if (!LAST) H[k] = hnew;
+            nh[m] = hnew;
             wet_out = wet_out & (hnew > tol) & (hnew < 1e150);
             double hn;
             if (AW && m < M - 1) {
@@ -321,11 +403,22 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                 }
                 hn = hn + dt * sm;
             }
-            HN[k] = hn;
-            HT[k] = HT[k] - lam * (fvr - fvl);
+            const double htn = HT[k] - lam * (fvr - fvl);
+            if (!LAST) {
+                HN[k] = hn;
+                HT[k] = htn;
+            }
+            nn[m] = hn;
+            nt[m] = htn;
+        }
+        if (LAST) {
+            // hu/hv from the normal/transverse momenta of this direction
+            if (DIR == 0) post_cell<M>(nh, nn, nt, *post, r, c);
+            else post_cell<M>(nh, nt, nn, *post, r, c);
         }
     })
-    return __syncthreads_and(wet_out) != 0;}
+    return __syncthreads_and(wet_out) != 0;
+}
 
 
 template <int M, bool YFIRST>
@@ -419,85 +512,23 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const bool aw1 = sweep_tile<M, D1, true, false, false, true, false>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best);
     const bool aw2 = aw1 ? sweep_tile<M, D1, true, false, true, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best)
                          : sweep_tile<M, D1, true, false, false, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best);
+    // post-processing on the tile interior (physics.py:360-376), fused into
+    // the second sweep's update of exactly those cells
+    PostCtx pc;
+    pc.dst = dst;
+    pc.base = base;
+    pc.FS = FS;
+    pc.NX = pv.NX;
+    pc.tol = prm.dry_tolerance;
+    pc.coef = kc.coef;
+#pragma unroll
+    for (int m = 0; m < MLAMR_MAX_LAYERS; ++m) pc.negs[m] = 0.0;
+    pc.fixes = pc.repairs = 0;
     if (aw2)
-        sweep_tile<M, D2, false, true, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best);
+        sweep_tile<M, D2, false, true, true, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, &pc);
     else
-        sweep_tile<M, D2, false, false, false, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best);
+        sweep_tile<M, D2, false, false, false, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, &pc);
 
-    // post-processing on the tile interior (physics.py:360-376)
-    const double tol = prm.dry_tolerance;
-    double negs[M];
-#pragma unroll
-    for (int m = 0; m < M; ++m) negs[m] = 0.0;
-    long long fixes = 0, repairs = 0;
-    const double coef = kc.coef;
-    FOR_RECT(1, ny2 - 1, 1, nx2 - 1, {
-        const int k = r * PX + c;
-        double h[M], hu[M], hv[M];
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            h[m] = s.S[m][k];
-            hu[m] = s.S[M + m][k];
-            hv[m] = s.S[2 * M + m][k];
-            const double neg = np_min(h[m], 0.0);
-            negs[m] = negs[m] + neg;
-            if (neg < 0.0) h[m] = 0.0;
-        }
-        if (M == 2) {  // _blend_shear (physics.py:292-327)
-            const double h1 = h[0], h2 = h[1 % M];
-            if (h1 > tol && h2 > tol) {
-                const double hu1 = hu[0], hu2 = hu[1 % M], hv1 = hv[0], hv2 = hv[1 % M];
-                bool ok = true;
-                const double y1 = recip_nr(h1), y2 = recip_nr(h2);
-                double u1 = div_fast(hu1, h1, y1, ok), v1 = div_fast(hv1, h1, y1, ok);
-                double u2 = div_fast(hu2, h2, y2, ok), v2 = div_fast(hv2, h2, y2, ok);
-                if (!ok) {
-                    u1 = hu1 / h1;
-                    u2 = hu2 / h2;
-                    v1 = hv1 / h1;
-                    v2 = hv2 / h2;
-                }
-                const double du = u1 - u2, dv = v1 - v2;
-                const double shear2 = (du * du) + (dv * dv);
-                const double bound = coef * (h1 + h2);
-                if (shear2 > bound) {
-                    ++fixes;
-                    const double alpha = sqrt(bound / shear2);
-                    const double htot = h1 + h2;
-                    const double umean = (hu1 + hu2) / htot;
-                    const double vmean = (hv1 + hv2) / htot;
-                    hu[0] = h1 * (umean + alpha * (u1 - umean));
-                    hu[1 % M] = h2 * (umean + alpha * (u2 - umean));
-                    hv[0] = h1 * (vmean + alpha * (v1 - vmean));
-                    hv[1 % M] = h2 * (vmean + alpha * (v2 - vmean));
-                }
-            }
-        }
-        // restore_wet_prefix (state.py:125-145), then zero_dry_momenta (:104-110)
-#pragma unroll
-        for (int m = 1; m < M; ++m) {
-            if (h[m] > tol && h[m - 1] <= tol) {
-                ++repairs;
-                h[m - 1] = h[m - 1] + h[m];
-                hu[m - 1] = hu[m - 1] + hu[m];
-                hv[m - 1] = hv[m - 1] + hv[m];
-                h[m] = 0.0;
-                hu[m] = 0.0;
-                hv[m] = 0.0;
-            }
-        }
-        const int64_t gaddr = base + (int64_t)r * pv.NX + c;
-#pragma unroll
-        for (int m = 0; m < M; ++m) {
-            if (h[m] <= tol) {
-                hu[m] = 0.0;
-                hv[m] = 0.0;
-            }
-            dst[m * FS + gaddr] = h[m];
-            dst[(M + m) * FS + gaddr] = hu[m];
-            dst[(2 * M + m) * FS + gaddr] = hv[m];
-        }
-    })
     // per-tile partials in one fused pass: warp shuffles (fixed xor tree),
     // then warp 0 combines the NT/32 warp values in warp order -- the same
     // order on every run, so the sums are deterministic
@@ -505,9 +536,9 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const int lane = t & 31, warp = t >> 5;
     double v[M + 2];
 #pragma unroll
-    for (int m = 0; m < M; ++m) v[m] = negs[m];
-    v[M] = (double)fixes;
-    v[M + 1] = (double)repairs;
+    for (int m = 0; m < M; ++m) v[m] = pc.negs[m];
+    v[M] = (double)pc.fixes;
+    v[M + 1] = (double)pc.repairs;
     // negative-depth sums and counters are zero in almost every warp: the
     // shuffle tree runs only where one is not
     bool any = false;
