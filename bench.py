@@ -262,7 +262,12 @@ def b200_arm(args):
     achieved = (sum(byts) / sum(durs)) / 1e9 if durs else None
     step_share = sum(durs) / (ms * 1e-3) if durs else None
     sim.step_timer_level = None
-    finest = sim.levels[L]
+    pool_bytes = sum(p.state.numel() * 8 * 2 + p.bathy.numel() * 8 for p in sim.levels.values())
+    patches_per_level = ({str(k): int(len(v)) for k, v in sim.layout.items()}
+                         if world > 1 else {str(k): v.P for k, v in sim.levels.items()})
+    cells_per_level = {str(k): v.ncells for k, v in sim.levels.items()}
+    host_ms = {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}
+    xbytes = int((getattr(sim, "bytes_exchanged", 0) - xbytes0) / args.steps)
 
     # ---- e2e: host buffers -> device -> K steps -> host ---------------------
     e2e = None
@@ -271,6 +276,12 @@ def b200_arm(args):
                "unavailable": "sharded snapshot/restore not implemented yet"}
     if not args.no_e2e and world == 1:
         snap = sim.snapshot()
+        # the user's checkpoint/restore cycle in one process: the source
+        # simulation hands its device buffers back for the restored one
+        sim.close()
+        del sim
+        import gc
+        gc.collect()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -303,7 +314,6 @@ def b200_arm(args):
                "sample": f"{desc}; 1 coarse step (all levels), oracle/ C+numpy port, {t:.1f} s"}
 
     if rank == 0:
-        pool_bytes = sum(p.state.numel() * 8 * 2 + p.bathy.numel() * 8 for p in sim.levels.values())
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
@@ -311,16 +321,14 @@ def b200_arm(args):
             "data": "synthetic",
             "config": {"workload": f"{args.config}: {pb.num_levels} levels, M={M}, "
                                    f"L1 {pb.coarse_nx}x{pb.coarse_ny}, ratios {pb.ratios_x}",
-                       "patches_per_level": ({str(k): int(len(v)) for k, v in sim.layout.items()}
-                                             if world > 1 else {str(k): v.P for k, v in sim.levels.items()}),
-                       "cells_per_level": {str(k): v.ncells for k, v in sim.levels.items()},
+                       "patches_per_level": patches_per_level,
+                       "cells_per_level": cells_per_level,
                        "parallelism": (f"SFC-sharded patches x{world} (NCCL shadow exchange)"
                                        if world > 1 else "single GPU"),
                        "l2": (f"inputs larger than L2 (device state {pool_bytes / 1e9:.2f} GB)" if pool_bytes > 126e6 else f"device state {pool_bytes / 1e9:.3f} GB fits in L2 (no flush)"),
                        "dt_policy": "reference: level-1 stable_dt, r_t subcycling",
-                       **({"exchange_bytes_per_step_rank0": int((sim.bytes_exchanged - xbytes0) / args.steps)}
-                          if world > 1 else {}),
-                       "host_ms_per_step": {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}},
+                       **({"exchange_bytes_per_step_rank0": xbytes} if world > 1 else {}),
+                       "host_ms_per_step": host_ms},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_over_algorithmic": traffic_ratio,
