@@ -245,6 +245,19 @@ int mlamr_level_reduce(mlamr_level lv, const double *interior_state,
                        int32_t *status, const int32_t *patch_list, int n_list,
                        void *stream);
 
+/* As mlamr_level_reduce, for a level whose sibling ghost cells were never
+ * copied because its step read them through the ghost plan (mlamr_step with
+ * ghost_base/ghost_plan): frame cells with a plan entry >= 0 are checked at
+ * that sibling cell of `ghost_state` -- the value the copy would have
+ * written -- so the non-finite scan covers the same values as the
+ * reference's isfinite over whole patch arrays (driver.py:286-297). */
+int mlamr_level_reduce_planned(mlamr_level lv, const double *interior_state,
+                               const double *ghost_state, const int32_t *child,
+                               double *patch_mass, int blocks_per_patch,
+                               int32_t *status, const int32_t *patch_list,
+                               int n_list, const int64_t *ghost_base,
+                               const int64_t *ghost_plan, void *stream);
+
 /* Reference flag rule, per-cell part (regrid.flag_cells, regrid.py:58-101):
  * cell_bits over the level index space (no frame): bit0 amplitude flag
  * |eta_m - eta_rest_m| > wave_tol_m, bit(1+m) layer m wet, bit7 covered.

@@ -206,29 +206,92 @@ __global__ void __launch_bounds__(NTA) k_ghost_plan(mlamr_level lv, const int64_
     }
 }
 
-// sibling copies: one thread per (ghost cell, patch); a single plan load
-// precedes the 3M independent loads.
+// sibling copies (ghost.py:186-196): one CTA of NTC threads per patch.  A
+// thread moves ghost cells in PAIRS -- consecutive plan entries are
+// neighbouring cells of a frame row (or the two cells of a side band on one
+// row), and their sibling sources are neighbours in the sibling's interior
+// -- so an aligned pair is one 16-byte load and store per plane.  Each
+// thread takes two pairs per round and issues all plan loads, then all
+// source loads, then the stores: the kernel is latency-bound (a plan load,
+// then the dependent data loads), so independent pairs in flight are what
+// reaches the bandwidth.
+constexpr int NTC = 128;
+
+// ghost index of an even idx -> (J, I) of the pair's first cell and whether
+// the second cell is its right neighbour in memory (ghost_cell_of order)
+__device__ __forceinline__ bool ghost_pair_of(int idx, int NX, int NY, int &J, int &I) {
+    if (idx < 4 * NX) {  // bottom rows, then top rows
+        const int q = idx < 2 * NX ? idx : idx - 2 * NX;
+        const int r = q / NX;
+        J = idx < 2 * NX ? r : NY - 2 + r;
+        I = q - r * NX;
+        return I + 1 < NX;
+    }
+    const int q = idx - 4 * NX;  // side bands: (0, 1) then (NX-2, NX-1) per row
+    J = MLAMR_G + (q >> 2);
+    I = (q & 2) ? NX - 2 : 0;
+    return true;
+}
+
 template <int M>
-__global__ void __launch_bounds__(NTA) k_fill_copy(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
+__global__ void __launch_bounds__(NTC) k_fill_copy(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
                                                    const int32_t *plist, const int32_t *status) {
     if (status != nullptr && *status != 0) return;
-    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+    const int p = plist ? plist[blockIdx.x] : (int)blockIdx.x;
     const int32_t *b = lv.box + 4 * p;
-    const int NX = b[2] - b[0] + 1 + 2 * MLAMR_G, ny = b[3] - b[1] + 1;
-    const int nghost = 4 * NX + 4 * ny;
+    const int NX = b[2] - b[0] + 1 + 2 * MLAMR_G, ny = b[3] - b[1] + 1, NY = ny + 2 * MLAMR_G;
+    const int npair = 2 * NX + 2 * ny;  // nghost / 2 (nghost = 4 NX + 4 ny)
     const int64_t FS = lv.field_stride;
     const int64_t off = lv.offset[p];
-    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nghost; idx += gridDim.x * NTA) {
-        const int64_t src = plan[gbase[p] + idx];
-        if (src < 0) continue;
-        int J, I;
-        ghost_cell_of(idx, NX, ny + 2 * MLAMR_G, ny, J, I);
-        const int64_t k = off + (int64_t)J * NX + I;
-        double v[3 * M];
+    const int64_t *pl = plan + gbase[p];
+    double *st = lv.state;
+    for (int q0 = threadIdx.x; q0 < npair; q0 += 2 * NTC) {
+        int64_t src[2][2], dst[2][2];
+        bool vec[2];
 #pragma unroll
-        for (int q = 0; q < 3 * M; ++q) v[q] = lv.state[q * FS + src];
+        for (int u = 0; u < 2; ++u) {
+            const int q = q0 + u * NTC;
+            const bool in = q < npair;
+            const int idx = 2 * (in ? q : q0);
+            src[u][0] = in ? pl[idx] : -1;
+            src[u][1] = in ? pl[idx + 1] : -1;
+            int J, I;
+            const bool adj = ghost_pair_of(idx, NX, NY, J, I);
+            dst[u][0] = off + (int64_t)J * NX + I;
+            if (adj) {
+                dst[u][1] = dst[u][0] + 1;
+            } else {
+                int J1, I1;
+                ghost_cell_of(idx + 1, NX, NY, ny, J1, I1);
+                dst[u][1] = off + (int64_t)J1 * NX + I1;
+            }
+            vec[u] = adj && src[u][0] >= 0 && src[u][1] == src[u][0] + 1 && ((dst[u][0] | src[u][0]) & 1) == 0;
+        }
+        double2 v[2][3 * M];
 #pragma unroll
-        for (int q = 0; q < 3 * M; ++q) lv.state[q * FS + k] = v[q];
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+            for (int k = 0; k < 3 * M; ++k) {
+                if (vec[u]) {
+                    v[u][k] = *reinterpret_cast<const double2 *>(st + k * FS + src[u][0]);
+                } else {
+                    v[u][k].x = src[u][0] >= 0 ? st[k * FS + src[u][0]] : 0.0;
+                    v[u][k].y = src[u][1] >= 0 ? st[k * FS + src[u][1]] : 0.0;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+#pragma unroll
+            for (int k = 0; k < 3 * M; ++k) {
+                if (vec[u]) {
+                    *reinterpret_cast<double2 *>(st + k * FS + dst[u][0]) = v[u][k];
+                } else {
+                    if (src[u][0] >= 0) st[k * FS + dst[u][0]] = v[u][k].x;
+                    if (src[u][1] >= 0) st[k * FS + dst[u][1]] = v[u][k].y;
+                }
+            }
+        }
     }
 }
 
@@ -651,7 +714,8 @@ template <int M>
 __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const double *interior,
                                                       const double *ghosts, const int32_t *child,
                                                       int child_rx, int child_ry, double *patch_mass,
-                                                      int32_t *status, const int32_t *plist) {
+                                                      int32_t *status, const int32_t *plist,
+                                                      const int64_t *gbase, const int64_t *plan) {
     __shared__ double red[NTA];
     __shared__ int bad;
     const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
@@ -668,8 +732,19 @@ __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const doub
         const bool inner = J >= MLAMR_G && J < pv.NY - MLAMR_G && I >= MLAMR_G && I < pv.NX - MLAMR_G;
         const double *st = inner ? interior : ghosts;
         const int64_t k = pv.off + idx;
+        int64_t kc = k;
+        if (!inner && plan != nullptr) {
+            // frame whose sibling cells the step read through the ghost plan
+            // (fused sibling fill): check the sibling cell the copy would
+            // have brought in
+            const int gi = (J < MLAMR_G) ? J * pv.NX + I
+                         : (J >= pv.NY - MLAMR_G) ? 2 * pv.NX + (J - (pv.NY - MLAMR_G)) * pv.NX + I
+                         : 4 * pv.NX + (J - MLAMR_G) * 4 + (I < MLAMR_G ? I : I - pv.NX + 4);
+            const int64_t v = plan[gbase[p] + gi];
+            if (v >= 0) kc = v;
+        }
         for (int q = 0; q < 3 * M; ++q)
-            if (!isfinite(st[q * FS + k])) nonfinite = 1;
+            if (!isfinite(st[q * FS + kc])) nonfinite = 1;
         if (inner) {
             const int gi = pv.lo_i + I - MLAMR_G, gj = pv.lo_j + J - MLAMR_G;
             const bool covered = child != nullptr && owner_at(child, lv.level_nx, lv.level_ny, gi, gj) >= 0;
@@ -859,10 +934,7 @@ extern "C" int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *pare
     const int4 b = make_int4(bcs[0], bcs[1], bcs[2], bcs[3]);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        if (nb > 0) {
-            dim3 grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), (unsigned)nb);
-            k_fill_copy<M><<<grid, NTA, 0, st>>>(lv, gbase, plan, patch_list, status);
-        }
+        if (nb > 0) k_fill_copy<M><<<nb, NTC, 0, st>>>(lv, gbase, plan, patch_list, status);
         if (parent != nullptr && n_interp > 0) {
             const int blocks = (int)std::min<int64_t>((n_interp + NTA - 1) / NTA, 148 * 32);
             k_fill_interp<M><<<blocks, NTA, 0, st>>>(lv, *parent, parent_old_state, theta, r_x, r_y,
@@ -999,6 +1071,15 @@ extern "C" int mlamr_interpolate_box(int M, const double *ch, const double *chu,
 extern "C" int mlamr_level_reduce(mlamr_level lv, const double *interior_state, const double *ghost_state,
                                   const int32_t *child, double *patch_mass, int blocks_per_patch,
                                   int32_t *status, const int32_t *patch_list, int n_list, void *stream) {
+    return mlamr_level_reduce_planned(lv, interior_state, ghost_state, child, patch_mass, blocks_per_patch,
+                                      status, patch_list, n_list, nullptr, nullptr, stream);
+}
+
+extern "C" int mlamr_level_reduce_planned(mlamr_level lv, const double *interior_state,
+                                          const double *ghost_state, const int32_t *child, double *patch_mass,
+                                          int blocks_per_patch, int32_t *status, const int32_t *patch_list,
+                                          int n_list, const int64_t *ghost_base, const int64_t *ghost_plan,
+                                          void *stream) {
     const int nb = patch_list ? n_list : lv.num_patches;
     if (nb <= 0) return 0;
     dim3 grid(blocks_per_patch, nb);
@@ -1006,7 +1087,8 @@ extern "C" int mlamr_level_reduce(mlamr_level lv, const double *interior_state, 
     int rc = dispatch_m(lv.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
         k_level_reduce<M><<<grid, NTA, 0, st>>>(lv, interior_state, ghost_state, child, 1, 1, patch_mass,
-                                                status, patch_list);
+                                                status, patch_list, ghost_plan ? ghost_base : nullptr,
+                                                ghost_plan);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();

@@ -453,7 +453,8 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         constexpr int NITEM = (NPAD + NT - 1) / NT;
         unsigned sa[NITEM];
         const double *ga[NITEM];
-        bool in[NITEM];
+        bool in[NITEM], fr[NITEM];
+        int64_t gv[NITEM];
 #pragma unroll
         for (int i = 0; i < NITEM; ++i) {
             const int idx = t + i * NT;
@@ -461,6 +462,8 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
             in[i] = idx < ny2 * PX && c < nx2;
             sa[i] = (unsigned)__cvta_generic_to_shared(&s.S[0][0]) + idx * 8;
             ga[i] = src + base + (int64_t)r * pv.NX + c;
+            fr[i] = false;
+            gv[i] = -1;
             if (gplan != nullptr && in[i]) {
                 // halo cell in the patch's ghost frame: with a ghost plan the
                 // sibling copy is fused into this staging -- read the covering
@@ -476,20 +479,35 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
                         gi = 2 * pv.NX + (J - (pv.NY - MLAMR_G)) * pv.NX + I;
                     else
                         gi = 4 * pv.NX + (J - MLAMR_G) * 4 + (I < MLAMR_G ? I : I - pv.NX + 4);
-                    const int64_t v = gplan[gbase[p] + gi];
-                    if (v >= 0) ga[i] = src + v;
+                    fr[i] = true;
+                    gv[i] = gplan[gbase[p] + gi];
                 }
             }
         }
         const int64_t boff = lv.bathy - src;  // same patch layout, one plane
+        // cells whose address is known go first; the frame cells' plan
+        // lookups (dependent loads) complete behind them
 #pragma unroll
         for (int q = 0; q < 3 * M + 1; ++q) {
             const int64_t po = (q < 3 * M) ? q * FS : boff;
 #pragma unroll
             for (int i = 0; i < NITEM; ++i)
-                if (in[i])
+                if (in[i] && !fr[i])
                     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa[i] + q * NPAD * 8),
                                  "l"(ga[i] + po));
+        }
+        if (gplan != nullptr) {
+#pragma unroll
+            for (int i = 0; i < NITEM; ++i) {
+                if (!fr[i]) continue;
+                const double *gs = gv[i] >= 0 ? src + gv[i] : ga[i];
+#pragma unroll
+                for (int q = 0; q < 3 * M + 1; ++q) {
+                    // bathymetry always from the patch's own frame
+                    const double *a = (q < 3 * M) ? gs + q * FS : ga[i] + boff;
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa[i] + q * NPAD * 8), "l"(a));
+                }
+            }
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);

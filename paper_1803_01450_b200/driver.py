@@ -26,6 +26,7 @@ composite mass) plus once per regrid (flag map).
 from __future__ import annotations
 
 import ctypes
+import os
 import time
 from collections import defaultdict
 from contextlib import contextmanager
@@ -166,10 +167,12 @@ class Simulation:
         self._flagbuf = {}
         self._scratch_bufs = {}
         # childless levels: sibling ghost copy inside the step's staging
-        # (mlamr_step with a ghost plan).  Off by default: on C4 it saves the
-        # 0.31 ms copy per finest fill but the plan lookups add ~0.3 ms of
-        # dependent-load latency to each step launch (profiles/r01/README.md)
-        self.fuse_sibling_fill = False
+        # (mlamr_step with a ghost plan; the finite check then reads those
+        # cells through the plan too).  On C4 it drops the 0.29 ms sibling
+        # copy per finest fill for ~0.19 ms of plan lookups per step launch
+        # (issued behind the tile's other loads): 70.9 -> 68.7 ms per coarse
+        # step.  MLAMR_FUSE_SIBLING=0 restores the separate copy.
+        self.fuse_sibling_fill = os.environ.get("MLAMR_FUSE_SIBLING", "1") == "1"
         self.levels: dict[int, LevelPool] = {}
         self.steps = {s.level: 0 for s in self.specs}
         self._stash = {}
@@ -260,8 +263,13 @@ class Simulation:
             ghosts = pool.state if pool.ghosts_in_cur else pool.other
             child = pool.child.data_ptr() if pool.child is not None else None
             pl, nl = pool.work_list()
-            self._call(self.lib.mlamr_level_reduce, pool.struct(), pool.state.data_ptr(), ghosts.data_ptr(),
-                       child, part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
+            gb = gp = None
+            if getattr(pool, "fused_frame", False) and not pool.ghosts_in_cur:
+                gbase, plan = pool.ghost_plan()[:2]
+                gb, gp = gbase.data_ptr(), plan.data_ptr()
+            self._call(self.lib.mlamr_level_reduce_planned, pool.struct(), pool.state.data_ptr(),
+                       ghosts.data_ptr(), child, part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, gb, gp,
+                       self.sh)
             s = self.spec(level)
             return part.view(-1, self.M).sum(dim=0) * (s.dx * s.dy)
 
@@ -618,6 +626,7 @@ class Simulation:
         # step: the sibling part of the fill is fused into the step
         fuse = self.fuse_sibling_fill and not has_child
         self.fill_level_ghosts(level, t0, siblings=not fuse)
+        self.levels[level].fused_frame = fuse   # the finite check reads its sibling cells via the plan
         self._step_patches(level, dt, fused_siblings=fuse)
         self.steps[level] += 1
         t1 = t0 + dt

@@ -396,6 +396,7 @@ class ShardedSimulation(Simulation):
         has_child = child is not None and len(self.layout.get(level + 1, _EMPTY)) > 0
         fuse = self.fuse_sibling_fill and not has_child
         self.fill_level_ghosts(level, t0, siblings=not fuse)
+        self.levels[level].fused_frame = fuse   # the finite check reads its sibling cells via the plan
         self._refresh(level)                                            # (ii)
         pool = self.levels[level]
         self._step_patches(level, dt, fused_siblings=fuse)

@@ -105,14 +105,15 @@ def test_config_run_matches_oracle(oracle, name):
     np.testing.assert_allclose(gpu.composite_mass(), mass, rtol=1e-12)
 
 
-def test_shelf_small_with_fused_sibling_fill_matches_reference():
-    """The step reading sibling halo cells through the ghost plan (instead
-    of a separate sibling copy) gives the same bits."""
+def test_shelf_small_with_separate_sibling_copy_matches_reference():
+    """The separate sibling-copy fill of the finest level (instead of the
+    default: the step reading sibling halo cells through the ghost plan)
+    gives the same bits."""
     from shelf_problem import shelf_problem
     from paper_1803_01450_b200.driver import Simulation
     z = load_golden("run_shelf_small.npz")
     sim = Simulation(shelf_problem())
-    sim.fuse_sibling_fill = True
+    sim.fuse_sibling_fill = False
     for dtref in z["dts"]:
         dt = sim.choose_dt()
         assert dt == float(dtref)

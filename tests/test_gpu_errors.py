@@ -99,3 +99,48 @@ def test_empty_child_level_runs():
     assert sim.levels.get(2) is None or sim.levels[2].P == 0
     sim.advance_coarse_step(sim.choose_dt())
     assert sim.stats.total_cell_updates == 128 * 128
+
+
+def test_nonfinite_check_reads_fused_sibling_ghosts_through_the_plan():
+    """With the sibling fill fused into the finest level's step, the finite
+    check (driver.py:286-297, isfinite over whole patch arrays) must see the
+    sibling value a copy would have put in the ghost cell: a NaN in that
+    sibling cell of the ghost-source buffer aborts, a NaN in the never-copied
+    (stale) frame cell does not."""
+    import torch
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+    from paper_1803_01450_b200.errors import NumericalAbortError
+    sim = Simulation(problems.config2(n_coarse_steps=1))   # 8x8 tiling: siblings everywhere
+    assert sim.fuse_sibling_fill
+    sim.advance_coarse_step(sim.choose_dt())
+    pool = sim.levels[sim.L]
+    assert getattr(pool, "fused_frame", False) and not pool.ghosts_in_cur
+    gbase, plan = (t.cpu().numpy() for t in pool.ghost_plan()[:2])
+    g = int(np.flatnonzero(plan >= 0)[0])
+    p = int(np.searchsorted(gbase, g, side="right") - 1)
+    idx = g - int(gbase[p])
+    b = pool.boxes[p]
+    NX, NY = int(b[2] - b[0] + 5), int(b[3] - b[1] + 5)
+    if idx < 2 * NX:
+        J, I = divmod(idx, NX)
+    elif idx < 4 * NX:
+        J, I = divmod(idx - 2 * NX, NX)
+        J += NY - 2
+    else:
+        q = idx - 4 * NX
+        J, s = 2 + q // 4, q % 4
+        I = (0, 1, NX - 2, NX - 1)[s]
+    frame_cell = int(pool.offsets[p]) + J * NX + I
+    # stale frame cell: not a ghost value of the fused path
+    keep = pool.other[frame_cell].item()
+    pool.other[frame_cell] = float("nan")
+    sim.composite_mass()
+    sim._sync_status("stale frame")
+    pool.other[frame_cell] = keep
+    # the sibling cell the copy would have read
+    pool.other[int(plan[g])] = float("nan")
+    torch.cuda.synchronize()
+    sim.composite_mass()
+    with pytest.raises(NumericalAbortError):
+        sim._sync_status("sibling source")
