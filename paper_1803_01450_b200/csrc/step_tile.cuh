@@ -82,7 +82,24 @@ __device__ __forceinline__ void post_cell(double (&h)[M], double (&hu)[M], doubl
     }
     if (M == 2) {  // _blend_shear (physics.py:292-327)
         const double h1 = h[0], h2 = h[1 % M];
-        if (h1 > tol && h2 > tol) {
+        // Screen: U >= shear2 / (1 + 2^-18) is built from approximate
+        // reciprocals (rcp.approx, relative error far below 1/8), so
+        // U * 1.125 < bound proves the reference's `shear2 > bound` false
+        // and the blend a no-op -- almost every co-wet cell, whose shear is
+        // orders of magnitude below g(1-r)(h1+h2).  Only cells the screen
+        // cannot clear take the exact divisions below.  NaN/inf operands
+        // fail the screen's comparison; h >= 1e300 (reciprocal below the
+        // normal range, flushed by .ftz) and coef <= 0 skip it.
+        bool maybe = true;
+        if (h1 > tol && h2 > tol && coef > 0.0 && h1 < 1e300 && h2 < 1e300) {
+            double a1, a2;
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(a1) : "d"(h1));
+            asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(a2) : "d"(h2));
+            const double su = fabs(hu[0]) * a1 + fabs(hu[1 % M]) * a2;
+            const double sv = fabs(hv[0]) * a1 + fabs(hv[1 % M]) * a2;
+            maybe = !((su * su + sv * sv) * 1.125 < coef * (h1 + h2));
+        }
+        if (maybe && h1 > tol && h2 > tol) {
             const double hu1 = hu[0], hu2 = hu[1 % M], hv1 = hv[0], hv2 = hv[1 % M];
             bool ok = true;
             const double y1 = recip_nr(h1), y2 = recip_nr(h2);
