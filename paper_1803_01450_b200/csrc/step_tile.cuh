@@ -174,7 +174,7 @@ __device__ __forceinline__ void post_cell(double (&h)[M], double (&hu)[M], doubl
 template <int M, int DIR, bool FIRST, bool AWA, bool AW, bool RUN_A, bool RUN_BC, bool LAST = false>
 __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
                            const mlamr_params &prm, const double (&rr)[4][4], double &best,
-                           PostCtx *post = nullptr) {
+                           double &nacc, PostCtx *post = nullptr) {
     // lam = dt / d and yd = recip_nr(d) come from the kernel prologue, where
     // their latency overlaps the tile's in-flight loads
     const double g = prm.gravity;
@@ -242,12 +242,17 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                 if (interior) {
                     // observed_max_speed (physics.py:261-278): speed = max(0, x_0,
                     // .., x_{M-1}) + cw with x_m = wet ? max(|hu|/h, |hv|/h) : 0 and
-                    // |hu|/h == |hu/h|.  Rounding is monotone, so
-                    // max_m(x_m) + cw == max_m(x_m + cw) and 0 + cw == cw: the
-                    // running max below is bit-identical to the reference's.
-                    const double x = wet ? np_max(fabs(u), fabs(v)) : 0.0;
-                    const double cand = (m == 0) ? np_max(cw, x + cw) : x + cw;
-                    best = (best < 0.0) ? cand : np_max(best, cand);
+                    // |hu|/h == |hu/h|.  Dry layers have u = v = 0 here, x_m >= 0,
+                    // and rounding is monotone, so max_m(x_m) + cw ==
+                    // max_m(x_m + cw) and max(cw, x_0 + cw) == x_0 + cw: the
+                    // running max is bit-identical to the reference's for
+                    // non-NaN operands.  fmax ignores NaN, so NaN-ness (numpy's
+                    // maximum propagates it) travels in `nacc`: |u| + |v| is NaN
+                    // iff either is (cw is finite or inf: hs > tol here), and the
+                    // tile maximum is replaced by NaN at the end.
+                    const double au = fabs(u), av = fabs(v);
+                    best = fmax(best, fmax(au, av) + cw);
+                    nacc = nacc + (au + av);
                 }
             }
         })
@@ -535,6 +540,7 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     __syncthreads();
 
     double best = -1.0;  // running observed speed over this thread's cells
+    double nacc = 0.0;   // NaN iff a speed operand was NaN
     // each sweep takes the all-wet path when every cell it reads is wet in
     // every layer (~90 % of C4's level-3 tiles)
     // phase A of the first sweep runs the general path and finds out
@@ -544,9 +550,9 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const double d1 = YFIRST ? lv.dy : lv.dx, d2 = YFIRST ? lv.dx : lv.dy;
     const double l1 = YFIRST ? lam_y : lam_x, l2 = YFIRST ? lam_x : lam_y;
     const double q1 = YFIRST ? y_y : y_x, q2 = YFIRST ? y_x : y_y;
-    const bool aw1 = sweep_tile<M, D1, true, false, false, true, false>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best);
-    const bool aw2 = aw1 ? sweep_tile<M, D1, true, false, true, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best)
-                         : sweep_tile<M, D1, true, false, false, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best);
+    const bool aw1 = sweep_tile<M, D1, true, false, false, true, false>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc);
+    const bool aw2 = aw1 ? sweep_tile<M, D1, true, false, true, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc)
+                         : sweep_tile<M, D1, true, false, false, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc);
     // post-processing on the tile interior (physics.py:360-376), fused into
     // the second sweep's update of exactly those cells
     PostCtx pc;
@@ -560,9 +566,9 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     for (int m = 0; m < MLAMR_MAX_LAYERS; ++m) pc.negs[m] = 0.0;
     pc.fixes = pc.repairs = 0;
     if (aw2)
-        sweep_tile<M, D2, false, true, true, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, &pc);
+        sweep_tile<M, D2, false, true, true, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, nacc, &pc);
     else
-        sweep_tile<M, D2, false, false, false, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, &pc);
+        sweep_tile<M, D2, false, false, false, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, nacc, &pc);
 
     // per-tile partials in one fused pass: warp shuffles (fixed xor tree),
     // then warp 0 combines the NT/32 warp values in warp order -- the same
@@ -592,6 +598,7 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     // speed max on the bit patterns: speeds are >= 0 (or NaN, canonicalised
     // above every finite value), and "no wet column" is -1, so the ordering
     // of the signed 64-bit patterns is the numpy maximum the reference takes
+    if (nacc != nacc) best = nacc;
     const long long mybits = (best < 0.0) ? -1LL
                            : ((best != best) ? 0x7ff8000000000000LL : __double_as_longlong(best));
     const int hi = __reduce_max_sync(0xffffffffu, (int)(mybits >> 32));

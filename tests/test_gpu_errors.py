@@ -144,3 +144,28 @@ def test_nonfinite_check_reads_fused_sibling_ghosts_through_the_plan():
     sim.composite_mass()
     with pytest.raises(NumericalAbortError):
         sim._sync_status("sibling source")
+
+
+def test_step_speed_is_nan_when_a_velocity_is_nan():
+    """observed_max_speed (physics.py:261-278) takes numpy maxima, which
+    propagate NaN: a NaN momentum in one wet interior cell makes that
+    patch's observed speed NaN (canonical bits), the others stay finite."""
+    import torch
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+    sim = Simulation(problems.config2(n_coarse_steps=1))
+    lev = sim.L
+    pool = sim.levels[lev]
+    assert pool.P > 1
+    sim.fill_level_ghosts(lev, sim.time)
+    b = pool.boxes[0]
+    NX = int(b[2] - b[0] + 5)
+    cell = int(pool.offsets[0]) + 5 * NX + 7            # interior cell (5, 7) of patch 0
+    M = sim.M
+    assert pool.state[cell].item() > sim.pb.dry_tolerance   # top layer wet there
+    pool.state[M * pool.FS + cell] = float("nan")          # hu of layer 0
+    torch.cuda.synchronize()
+    sim._step_patches(lev, 1e-3)
+    bits = pool.speed_bits[:pool.P].cpu().numpy()
+    assert bits[0] == 0x7FF8000000000000
+    assert np.all((bits[1:] >= 0) & (bits[1:] < 0x7FF0000000000000))
