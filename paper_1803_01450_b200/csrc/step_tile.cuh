@@ -36,13 +36,14 @@ struct StepSmem {
 // ops and saturated the XU pipe in the first profile) and consecutive
 // threads touch consecutive doubles (no bank conflicts in either sweep
 // direction).
-#define FOR_RECT(r0, r1, c0, c1, ...)                                    \
+// (a begin/end macro pair rather than a macro taking the body, so the
+// body keeps its own source lines in the profiler's source view)
+#define FOR_RECT_BEGIN(r0, r1, c0, c1)                                   \
     for (int idx_ = threadIdx.x; idx_ < ((r1) - (r0)) * PX; idx_ += NT) { \
         const int r = (r0) + idx_ / PX;                                  \
         const int c = idx_ - (idx_ / PX) * PX;                           \
-        if (c < (c0) || c >= (c1)) continue;                             \
-        __VA_ARGS__                                                      \
-    }
+        if (c < (c0) || c >= (c1)) continue;
+#define FOR_RECT_END }
 
 
 // Reconstruction bottoms of layer m at a cell (physics.py:200-207, 105-110):
@@ -195,7 +196,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     if (RUN_A) {
         bool wet_in = true;
         // ---- Phase A: per-cell inputs on the pre-sweep state of this direction
-        FOR_RECT(lr0, lr1, lc0, lc1, {
+        FOR_RECT_BEGIN(lr0, lr1, lc0, lc1)
             const int k = r * PX + c;
             double h[M];
             double hs = 0.0;
@@ -255,13 +256,13 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     nacc = nacc + (au + av);
                 }
             }
-        })
+        FOR_RECT_END
         const bool all_in = __syncthreads_and(wet_in) != 0;
         if (!RUN_BC) return all_in;
     }
 
     // ---- Phase B: HLL fluxes per interface (physics.py:101-161) + sources
-    FOR_RECT(lr0, fr1, lc0, fc1, {
+    FOR_RECT_BEGIN(lr0, fr1, lc0, fc1)
         const int kl = r * PX + c;
         const int kr = kl + STEP;
         const bool cop = AW || (s.cowet[kl] && s.cowet[kr]);
@@ -362,7 +363,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                 s.src[m - 1][k] = acc;
             }
         }
-    })
+    FOR_RECT_END
     __syncthreads();
 
     // ---- Phase C: conservative update + pressure correction + source.
@@ -370,7 +371,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     // their wetness decides (block-wide, with the closing barrier) whether
     // that sweep can take the all-wet path.
     bool wet_out = true;
-    FOR_RECT(ur0, ur1, uc0, uc1, {
+    FOR_RECT_BEGIN(ur0, ur1, uc0, uc1)
         const int k = r * PX + c;
         const int km = k - STEP, kp = k + STEP;
         const bool copl = AW || (s.cowet[km] && s.cowet[k]);
@@ -438,7 +439,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             if (DIR == 0) post_cell<M>(nh, nn, nt, *post, r, c);
             else post_cell<M>(nh, nt, nn, *post, r, c);
         }
-    })
+    FOR_RECT_END
     return __syncthreads_and(wet_out) != 0;
 }
 
@@ -721,6 +722,7 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
     return (int)cudaGetLastError();
 }
 
-#undef FOR_RECT
+#undef FOR_RECT_BEGIN
+#undef FOR_RECT_END
 
 }  // namespace MLAMR_STEP_NS
