@@ -385,9 +385,12 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             const double h0 = H[k];
             const double fhl = s.F[2 * m][km], fhr = s.F[2 * m][k];
             const double fml = s.F[2 * m + 1][km], fmr = s.F[2 * m + 1][k];
-            // upwinded transverse flux (physics.py:155-161)
-            const double fvl = fhl > 0.0 ? fhl * s.v[m][km] : (fhl < 0.0 ? fhl * s.v[m][k] : 0.0);
-            const double fvr = fhr > 0.0 ? fhr * s.v[m][k] : (fhr < 0.0 ? fhr * s.v[m][kp] : 0.0);
+            // upwinded transverse flux (physics.py:155-161):
+            // f > 0 ? f * v_left : (f < 0 ? f * v_right : 0), branch-free
+            // (both neighbours' v loaded; f == +-0 or NaN gives +0)
+            const double vkm = s.v[m][km], vk = s.v[m][k], vkp = s.v[m][kp];
+            const double fvl = fabs(fhl) > 0.0 ? fhl * (fhl > 0.0 ? vkm : vk) : 0.0;
+            const double fvr = fabs(fhr) > 0.0 ? fhr * (fhr > 0.0 ? vk : vkp) : 0.0;
             const double hnew = h0 - lam * (fhr - fhl);
             if (!LAST) H[k] = hnew;
             nh[m] = hnew;
