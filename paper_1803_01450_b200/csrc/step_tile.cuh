@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
                                              double *tile_acc, const int32_t *status,
                                              const int64_t *__restrict__ gbase,
                                              const int64_t *__restrict__ gplan) {
-    if (status != nullptr && *status != 0) return;
+    // the status word is read now but tested only once this tile's staging
+    // is in flight: testing it first put a dependent global load in front
+    // of every CTA's loads
+    const int32_t st0 = status != nullptr ? *status : 0;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     StepSmem<M> &s = *reinterpret_cast<StepSmem<M> *>(smem_raw);
     const int t = threadIdx.x;
@@ -537,6 +540,10 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         }
     }
     asm volatile("cp.async.commit_group;\n" ::);
+    if (st0 != 0) {  // an earlier kernel raised an error: nothing to do
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        return;
+    }
     const double(&rr)[4][4] = kc.rr;
     const double lam_x = kc.lam_x, lam_y = kc.lam_y;
     const double y_x = recip_nr(lv.dx), y_y = recip_nr(lv.dy);
