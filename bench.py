@@ -271,13 +271,11 @@ def b200_arm(args):
 
     # ---- e2e: host buffers -> device -> K steps -> host ---------------------
     e2e = None
-    if world > 1:
-        e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None, "d2h_bytes_per_step": None,
-               "unavailable": "sharded snapshot/restore not implemented yet"}
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e:
         snap = sim.snapshot()
         # the user's checkpoint/restore cycle in one process: the source
         # simulation hands its device buffers back for the restored one
+        # (under sharding every rank snapshots and restores its own pools)
         sim.close()
         del sim
         import gc
@@ -286,7 +284,10 @@ def b200_arm(args):
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        sim2 = Simulation.restore(pb, snap, stream=stream)
+        if world > 1:
+            sim2 = ShardedSimulation.restore(pb, snap, stream=stream)
+        else:
+            sim2 = Simulation.restore(pb, snap, stream=stream)
         Simulation.release_snapshot(snap)   # its pinned buffers take the final snapshot
         c0 = sim2.stats.total_cell_updates
         for _ in range(args.steps):
@@ -294,15 +295,20 @@ def b200_arm(args):
         out = sim2.snapshot()
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
+        ce = (sim2.stats.total_cell_updates - c0) * M
+        hb, db = sim2.h2d_bytes, sim2.d2h_bytes
         if world > 1:
             tt = torch.tensor([te], dtype=torch.float64, device="cuda")
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt.item())
-        ce = (sim2.stats.total_cell_updates - c0) * M * world
+            cc = torch.tensor([ce, hb, db], dtype=torch.float64, device="cuda")
+            dist.all_reduce(cc, op=dist.ReduceOp.SUM)
+            ce, hb, db = (float(x) for x in cc.tolist())
         e2e = {"value": ce / te, "unit": UNIT,
-               "h2d_bytes_per_step": int(sim2.h2d_bytes / args.steps),
-               "d2h_bytes_per_step": int(sim2.d2h_bytes / args.steps),
-               "timed": "restore(host pinned state -> HBM) + K coarse steps + snapshot(HBM -> host)"}
+               "h2d_bytes_per_step": int(hb / args.steps),
+               "d2h_bytes_per_step": int(db / args.steps),
+               "timed": "restore(host pinned state -> HBM) + K coarse steps + snapshot(HBM -> host)"
+                        + (", every rank its own pools, max over ranks" if world > 1 else "")}
         del sim2, snap, out
 
     # ---- CPU baseline (rank 0, N=1 only) -------------------------------------
@@ -323,7 +329,7 @@ def b200_arm(args):
                                    f"L1 {pb.coarse_nx}x{pb.coarse_ny}, ratios {pb.ratios_x}",
                        "patches_per_level": patches_per_level,
                        "cells_per_level": cells_per_level,
-                       "parallelism": (f"SFC-sharded patches x{world} (NCCL shadow exchange)"
+                       "parallelism": (f"SFC-sharded patches x{world} ({dist.get_backend()} shadow exchange)"
                                        if world > 1 else "single GPU"),
                        "l2": (f"inputs larger than L2 (device state {pool_bytes / 1e9:.2f} GB)" if pool_bytes > 126e6 else f"device state {pool_bytes / 1e9:.3f} GB fits in L2 (no flush)"),
                        "dt_policy": "reference: level-1 stable_dt, r_t subcycling",

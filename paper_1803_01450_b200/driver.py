@@ -816,6 +816,14 @@ class Simulation:
         """Rebuild a device hierarchy from :meth:`snapshot` output (host->device)."""
         return cls(problem, device=device, stream=stream, _restore=snap, reserve_factor=reserve_factor)
 
+    def _restore_pool(self, lev: int, d: dict) -> LevelPool:
+        """An empty pool for a level of a snapshot (sharded runs add ownership)."""
+        return LevelPool(self.spec(lev), d["boxes"], self.M, self.dev, self.stream, need_gown=lev < self.L)
+
+    def _level_boxes(self, lev: int) -> np.ndarray:
+        """All boxes of a level (a sharded run's pools hold only some)."""
+        return self.levels[lev].boxes
+
     def _restore_from(self, snap: dict) -> None:
         self.time = snap["time"]
         self.steps = dict(snap["steps"])
@@ -824,7 +832,7 @@ class Simulation:
         nbytes = 0
         for lev in sorted(snap["levels"]):
             d = snap["levels"][lev]
-            pool = LevelPool(self.spec(lev), d["boxes"], self.M, self.dev, self.stream, need_gown=lev < self.L)
+            pool = self._restore_pool(lev, d)
             with torch.cuda.stream(self.stream):
                 pool.state.copy_(d["state"], non_blocking=True)
                 pool.bathy.copy_(d["bathy"], non_blocking=True)
@@ -835,7 +843,7 @@ class Simulation:
         for lev in range(1, self.L):
             if lev + 1 in self.levels:
                 s = self.spec(lev)
-                self.levels[lev].child = paint_child_map(s, self.levels[lev + 1].boxes, s.r_x, s.r_y,
+                self.levels[lev].child = paint_child_map(s, self._level_boxes(lev + 1), s.r_x, s.r_y,
                                                          self.dev, self.stream)
         with torch.cuda.stream(self.stream):
             self.acc.copy_(snap["acc"], non_blocking=True)

@@ -43,20 +43,14 @@ _EMPTY = np.zeros((0, 4), np.int64)
 
 class ShardedSimulation(Simulation):
     def __init__(self, problem, comm: Comm | None = None, device: str = "cuda", stream=None,
-                 reserve_factor: float = 1.0):
-        self.comm = comm or Comm()
-        self.rank, self.world = self.comm.rank, self.comm.world
-        self.layout, self.owner, self.held = {}, {}, {}
-        # per level and rank: the held patches needed in full (owned, parents,
-        # children); the other shadows are refreshed as interior rings
-        self.full = {}
-        self.ring_refresh = True
-        self._ring_cache = {}
-        self._fullc_cache = {}
-        self.bytes_exchanged = 0
+                 reserve_factor: float = 1.0, _restore: dict | None = None):
+        self._init_sharding(comm)
         self._common_init(problem, device, stream)
         if self.pb.flag_rule[0] == "gradient":
             raise NotImplementedError("sharded runs support the reference and Bernoulli flag rules")
+        if _restore is not None:
+            self._restore_from(_restore)
+            return
         b1 = boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)])
         self.layout[1] = b1
         self.owner[1] = np.zeros(1, np.int32)
@@ -72,6 +66,59 @@ class ShardedSimulation(Simulation):
         if reserve_factor > 0:
             from .device import reserve
             reserve(int(reserve_factor * self.device_bytes()), self.dev, self.stream)
+
+    def _init_sharding(self, comm) -> None:
+        self.comm = comm or Comm()
+        self.rank, self.world = self.comm.rank, self.comm.world
+        self.layout, self.owner, self.held = {}, {}, {}
+        # per level and rank: the held patches needed in full (owned, parents,
+        # children); the other shadows are refreshed as interior rings
+        self.full = {}
+        self.ring_refresh = True
+        self._ring_cache = {}
+        self._fullc_cache = {}
+        self.bytes_exchanged = 0
+
+    # -- checkpoint: per-rank snapshot of its pools (owned + shadows) -------------
+    def snapshot(self) -> dict:
+        """This rank's part of the hierarchy (Simulation.snapshot of its pools)
+        plus the global layouts and ownership, for restore() by the same
+        rank of a job of the same size."""
+        snap = super().snapshot()
+        cp = lambda d: {k: {r: a.copy() for r, a in v.items()} for k, v in d.items()}
+        snap["sharded"] = {
+            "world": self.world, "rank": self.rank,
+            "layout": {k: v.copy() for k, v in self.layout.items()},
+            "owner": {k: v.copy() for k, v in self.owner.items()},
+            "held": cp(self.held), "full": cp(self.full),
+            "local": {lev: (pool.gidx.copy(), None if pool.owned is None else pool.owned.copy())
+                      for lev, pool in self.levels.items()},
+        }
+        return snap
+
+    @classmethod
+    def restore(cls, problem, snap: dict, comm: Comm | None = None, device: str = "cuda",
+                stream=None) -> "ShardedSimulation":
+        return cls(problem, comm=comm, device=device, stream=stream, _restore=snap)
+
+    def _restore_from(self, snap: dict) -> None:
+        sh = snap["sharded"]
+        if sh["world"] != self.world or sh["rank"] != self.rank:
+            raise ValueError(f"snapshot of rank {sh['rank']}/{sh['world']} restored on rank {self.rank}/{self.world}")
+        self.layout = {k: v.copy() for k, v in sh["layout"].items()}
+        self.owner = {k: v.copy() for k, v in sh["owner"].items()}
+        self.held = {k: {r: a.copy() for r, a in v.items()} for k, v in sh["held"].items()}
+        self.full = {k: {r: a.copy() for r, a in v.items()} for k, v in sh["full"].items()}
+        self._restore_local = sh["local"]
+        super()._restore_from(snap)
+
+    def _restore_pool(self, lev: int, d: dict) -> LevelPool:
+        gidx, owned = self._restore_local[lev]
+        return LevelPool(self.spec(lev), d["boxes"], self.M, self.dev, self.stream, need_gown=lev < self.L,
+                         owned=owned, gidx=gidx)
+
+    def _level_boxes(self, lev: int) -> np.ndarray:
+        return self.layout[lev]
 
     # -- geometry helpers -----------------------------------------------------
     def _scale(self, level: int):

@@ -3,7 +3,9 @@
 Each rank runs the sharded driver over its share of the patches and, in the
 same process, the single-GPU driver over all of them; after every coarse
 step every owned patch must be bit-identical, and the all-reduced
-statistics must equal the single-GPU ones."""
+statistics must equal the single-GPU ones.  Halfway through, the sharded
+run is checkpointed (every rank its own pools) and continued from the
+restored copy."""
 
 import os
 import sys
@@ -64,6 +66,13 @@ def main():
 
     compare("init")
     for k in range(steps):
+        if k == steps // 2:
+            # checkpoint: every rank snapshots its own pools (owned +
+            # shadows); the restored sharded run continues bit-identically
+            snap = sh.snapshot()
+            sh.close()
+            sh = ShardedSimulation.restore(pb, snap, stream=torch.cuda.Stream())
+            compare(f"restored before step{k}")
         dt = ref.choose_dt()
         assert sh.choose_dt() == dt, k
         ref.apply_dynamic_rt(dt)
