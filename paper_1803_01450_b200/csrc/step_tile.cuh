@@ -620,14 +620,17 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         s.redi[warp] = (hi < 0) ? -1LL : (long long)(((unsigned long long)(unsigned)hi << 32) | lo);
     }
     __syncthreads();
-    if (t == 0) {
-        double *acc = tile_acc + (int64_t)tile * (M + 2);
-        for (int q = 0; q < M + 2; ++q) {
-            double a = s.red[q * NW];
-            for (int w = 1; w < NW; ++w) a = a + s.red[q * NW + w];
-            acc[q] = a;
-        }
+    // one lane per quantity (each sums its warp values in warp order, so
+    // the result is the serial sum's), the speed maximum on another warp:
+    // the CTA's tail is one short chain instead of M+3 serial ones
+    if (t < M + 2) {
+        double a = s.red[t * NW];
+#pragma unroll
+        for (int w = 1; w < NW; ++w) a = a + s.red[t * NW + w];
+        tile_acc[(int64_t)tile * (M + 2) + t] = a;
+    } else if (t == 32) {
         long long b = s.redi[0];
+#pragma unroll
         for (int w = 1; w < NW; ++w) b = max(b, s.redi[w]);
         if (b >= 0) atomicMax(speed_bits + p, b);
     }
