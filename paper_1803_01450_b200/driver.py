@@ -762,9 +762,12 @@ class Simulation:
         return self.stats
 
     # -- checkpoint: host snapshot / restore (pinned host buffers) ----------------------------
-    def snapshot(self) -> dict:
-        """Copy the whole hierarchy (current buffers incl. ghost frames,
-        bathymetry, layouts, clocks and counters) into pinned host memory."""
+    def snapshot(self, bathymetry: bool = False) -> dict:
+        """Copy the hierarchy (current buffers incl. ghost frames, layouts,
+        clocks and counters) into pinned host memory.  The pools'
+        bathymetry is problem data every pool derives on the device from
+        the problem's level arrays (mlamr_fill_bathymetry), so it is copied
+        only with ``bathymetry=True``; a restore re-derives it otherwise."""
         snap = {"time": self.time, "steps": dict(self.steps), "specs": list(self.specs), "levels": {},
                 "acc": None, "delta_acc": None, "mass_prev": np.array(self._mass_prev),
                 "stats": replace(self.stats)}
@@ -774,9 +777,11 @@ class Simulation:
             for lev, pool in self.levels.items():
                 st = pinned_acquire(pool.state.numel(), torch.float64).view(pool.state.shape)
                 st.copy_(pool.state, non_blocking=True)
-                ba = pinned_acquire(pool.bathy.numel(), torch.float64).view(pool.bathy.shape)
-                ba.copy_(pool.bathy, non_blocking=True)
-                nbytes += st.numel() * 8 + ba.numel() * 8
+                ba = None
+                if bathymetry:
+                    ba = pinned_acquire(pool.bathy.numel(), torch.float64).view(pool.bathy.shape)
+                    ba.copy_(pool.bathy, non_blocking=True)
+                nbytes += st.numel() * 8 + (ba.numel() * 8 if ba is not None else 0)
                 snap["levels"][lev] = {"boxes": pool.boxes.copy(), "state": st, "bathy": ba, "time": pool.time,
                                        "ghosts": pool.ghosts_in_cur}
             acc = torch.empty(self.acc.shape, dtype=torch.float64, pin_memory=True)
@@ -835,8 +840,12 @@ class Simulation:
             pool = self._restore_pool(lev, d)
             with torch.cuda.stream(self.stream):
                 pool.state.copy_(d["state"], non_blocking=True)
-                pool.bathy.copy_(d["bathy"], non_blocking=True)
-            nbytes += d["state"].numel() * 8 + d["bathy"].numel() * 8
+                if d["bathy"] is not None:
+                    pool.bathy.copy_(d["bathy"], non_blocking=True)
+            if d["bathy"] is None and pool.P:
+                self._call(self.lib.mlamr_fill_bathymetry, pool.struct(), self.level_bathy[lev - 1].data_ptr(),
+                           self.bcs, self.sh)
+            nbytes += d["state"].numel() * 8 + (d["bathy"].numel() * 8 if d["bathy"] is not None else 0)
             pool.time = d["time"]
             pool.ghosts_in_cur = d["ghosts"]
             self.levels[lev] = pool
