@@ -505,7 +505,13 @@ class Simulation:
         cb = np.asarray(cb, dtype=np.int64).reshape(-1, 4)
         nboxes = np.stack([cb[:, 0] * rx, cb[:, 1] * ry, (cb[:, 2] + 1) * rx - 1, (cb[:, 3] + 1) * ry - 1], 1)
         if old is not None:
-            if len(old.boxes) == len(nboxes) and np.array_equal(self._lexsorted(old.boxes), self._lexsorted(nboxes)):
+            # the reference keeps the old patches when the sorted box lists
+            # agree (regrid.py:265-268); an unchanged flag map gives the very
+            # same list (clustering is deterministic), so the direct
+            # comparison answers the common case without the sorts
+            if np.array_equal(old.boxes, nboxes) or (
+                    len(old.boxes) == len(nboxes)
+                    and np.array_equal(self._lexsorted(old.boxes), self._lexsorted(nboxes))):
                 return False
         elif len(nboxes) == 0:
             return False

@@ -362,8 +362,9 @@ class ShardedSimulation(Simulation):
         old_layout = self.layout.get(level + 1, _EMPTY)
         old_owner = self.owner.get(level + 1, np.zeros(0, np.int32))
         if level + 1 in self.levels:
-            if len(old_layout) == len(nboxes) and np.array_equal(self._lexsorted(old_layout),
-                                                                 self._lexsorted(nboxes)):
+            if np.array_equal(old_layout, nboxes) or (
+                    len(old_layout) == len(nboxes)
+                    and np.array_equal(self._lexsorted(old_layout), self._lexsorted(nboxes))):
                 return False
         elif len(nboxes) == 0:
             return False
