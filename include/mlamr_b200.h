@@ -272,6 +272,16 @@ int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_params prm,
  * stride = packed length); segments = int64 [n][3] (src offset, dst
  * offset, length).  Patch lists (patch_list/n_list) above restrict a launch
  * to the patches a rank owns; NULL = every patch of the pool. */
+/* Checkpoints: copy the interiors of every patch of a level (all 3M state
+ * planes of `state`) to `packed` (unpack = 0) or back (unpack = 1).
+ * packed is [3M][n_total], patch p's interior at pbase[p] (prefix sums of
+ * nx*ny), rows x-fastest.  Replaces copying whole buffers in
+ * Simulation.snapshot/restore: ghost frames and padding are refilled
+ * before use (driver.py:175-190 fills every level first in its advance). */
+int mlamr_pack_interiors(mlamr_level lv, double *state, double *packed,
+                         const int64_t *pbase, int64_t n_total, int max_interior,
+                         int unpack, void *stream);
+
 int mlamr_copy_segments(const double *src, int64_t src_stride, double *dst, int64_t dst_stride,
                         const int64_t *segments, int n_segments, int max_len, int nplanes,
                         void *stream);

@@ -89,6 +89,8 @@ SIGNATURES = {
                                              c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_level_reduce": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp,
                                           ctypes.c_int, c_vp]),
+    "mlamr_pack_interiors": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                            c_vp]),
     "mlamr_level_reduce_planned": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, c_vp,
                                                   ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_flag_cells": (ctypes.c_int, [Level, c_vp, Params, c_vp, c_vp, c_vp, ctypes.c_int, c_vp,

@@ -1131,6 +1131,40 @@ extern "C" int mlamr_copy_segments(const double *src, int64_t src_stride, double
     return (int)cudaGetLastError();
 }
 
+// Checkpoints (Simulation.snapshot / restore): the interiors of every patch
+// of a level, plane by plane, packed contiguously (patch order, rows
+// x-fastest; pbase = prefix sums of the interior sizes).  Ghost frames and
+// alignment padding are rebuilt before anything reads them (every level's
+// advance starts with its fill), so a checkpoint carries only these.
+__global__ void __launch_bounds__(NTA) k_pack_interiors(mlamr_level lv, double *state, double *packed,
+                                                        const int64_t *pbase, int64_t ntot, int nplanes,
+                                                        int unpack) {
+    const int p = blockIdx.y;
+    const PatchView pv = patch_view(lv, p);
+    const int n = pv.nx * pv.ny;
+    const int64_t pb = pbase[p];
+    const int64_t FS = lv.field_stride;
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < n; idx += gridDim.x * NTA) {
+        const int j = idx / pv.nx, i = idx - j * pv.nx;
+        const int64_t k = pv.off + (int64_t)(j + MLAMR_G) * pv.NX + (i + MLAMR_G);
+        for (int q = 0; q < nplanes; ++q) {
+            if (unpack)
+                state[q * FS + k] = packed[q * ntot + pb + idx];
+            else
+                packed[q * ntot + pb + idx] = state[q * FS + k];
+        }
+    }
+}
+
+extern "C" int mlamr_pack_interiors(mlamr_level lv, double *state, double *packed, const int64_t *pbase,
+                                    int64_t n_total, int max_interior, int unpack, void *stream) {
+    if (lv.num_patches <= 0) return 0;
+    dim3 grid((unsigned)std::max(1, std::min(4, (max_interior + NTA - 1) / NTA)), (unsigned)lv.num_patches);
+    k_pack_interiors<<<grid, NTA, 0, as_stream(stream)>>>(lv, state, packed, pbase, n_total, 3 * lv.num_layers,
+                                                          unpack);
+    return (int)cudaGetLastError();
+}
+
 // self-test of the shared-reciprocal division against div.rn.f64
 __global__ void k_selftest_div(const double *a, const double *b, int n, unsigned long long *bad,
                                unsigned long long *slow) {

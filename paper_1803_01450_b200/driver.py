@@ -36,7 +36,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import LevelPool, arena, empty_level_struct, paint_child_map, release
+from .device import LevelPool, acquire, arena, empty_level_struct, paint_child_map, release
 from .errors import CflViolationError, NumericalAbortError, TimeSyncError, raise_status
 from .mesh import GHOST_WIDTH, IndexBox, LevelSpec, boxes_array, paint
 from .regrid import chop_boxes, cluster_boxes, cluster_boxes_device, nesting_allowed
@@ -768,12 +768,21 @@ class Simulation:
         return self.stats
 
     # -- checkpoint: host snapshot / restore (pinned host buffers) ----------------------------
+    def _interior_base(self, pool: LevelPool):
+        """(device prefix sums of the patches' interior sizes, total)."""
+        b = pool.boxes
+        n = (b[:, 2] - b[:, 0] + 1) * (b[:, 3] - b[:, 1] + 1) if pool.P else np.zeros(0, np.int64)
+        base = np.concatenate([[0], np.cumsum(n)[:-1]]).astype(np.int64) if pool.P else np.zeros(1, np.int64)
+        return arena().upload(base, self.dev, self.stream), int(n.sum()) if pool.P else 0
+
     def snapshot(self, bathymetry: bool = False) -> dict:
-        """Copy the hierarchy (current buffers incl. ghost frames, layouts,
-        clocks and counters) into pinned host memory.  The pools'
-        bathymetry is problem data every pool derives on the device from
-        the problem's level arrays (mlamr_fill_bathymetry), so it is copied
-        only with ``bathymetry=True``; a restore re-derives it otherwise."""
+        """Copy the hierarchy (the patches' interiors, layouts, clocks and
+        counters) into pinned host memory.  Ghost frames are refilled before
+        anything reads them, so only interiors are packed
+        (mlamr_pack_interiors).  The pools' bathymetry is problem data every
+        pool derives on the device from the problem's level arrays
+        (mlamr_fill_bathymetry), so it is copied only with
+        ``bathymetry=True``; a restore re-derives it otherwise."""
         snap = {"time": self.time, "steps": dict(self.steps), "specs": list(self.specs), "levels": {},
                 "acc": None, "delta_acc": None, "mass_prev": np.array(self._mass_prev),
                 "stats": replace(self.stats)}
@@ -781,15 +790,22 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             from .device import pinned_acquire
             for lev, pool in self.levels.items():
-                st = pinned_acquire(pool.state.numel(), torch.float64).view(pool.state.shape)
-                st.copy_(pool.state, non_blocking=True)
+                pbase, ntot = self._interior_base(pool)
+                n3 = 3 * self.M * max(ntot, 1)
+                packed = acquire(n3, torch.float64, self.dev, self.stream)
+                self._call(self.lib.mlamr_pack_interiors, pool.struct(), pool.state.data_ptr(), packed.data_ptr(),
+                           pbase.data_ptr(), max(ntot, 1), pool.max_interior, 0, self.sh)
+                st = pinned_acquire(n3, torch.float64)
+                st.copy_(packed, non_blocking=True)
+                release(packed)
                 ba = None
                 if bathymetry:
                     ba = pinned_acquire(pool.bathy.numel(), torch.float64).view(pool.bathy.shape)
                     ba.copy_(pool.bathy, non_blocking=True)
                 nbytes += st.numel() * 8 + (ba.numel() * 8 if ba is not None else 0)
+                # interiors only: a restored pool's frames are refilled first
                 snap["levels"][lev] = {"boxes": pool.boxes.copy(), "state": st, "bathy": ba, "time": pool.time,
-                                       "ghosts": pool.ghosts_in_cur}
+                                       "ghosts": False}
             acc = torch.empty(self.acc.shape, dtype=torch.float64, pin_memory=True)
             acc.copy_(self.acc, non_blocking=True)
             dacc = torch.empty(self.delta_acc.shape, dtype=torch.float64, pin_memory=True)
@@ -845,7 +861,12 @@ class Simulation:
             d = snap["levels"][lev]
             pool = self._restore_pool(lev, d)
             with torch.cuda.stream(self.stream):
-                pool.state.copy_(d["state"], non_blocking=True)
+                pbase, ntot = self._interior_base(pool)
+                packed = acquire(d["state"].numel(), torch.float64, self.dev, self.stream)
+                packed.copy_(d["state"], non_blocking=True)
+                self._call(self.lib.mlamr_pack_interiors, pool.struct(), pool.state.data_ptr(), packed.data_ptr(),
+                           pbase.data_ptr(), max(ntot, 1), pool.max_interior, 1, self.sh)
+                release(packed)
                 if d["bathy"] is not None:
                     pool.bathy.copy_(d["bathy"], non_blocking=True)
             if d["bathy"] is None and pool.P:
