@@ -78,7 +78,19 @@ __device__ void bc_side(double *st, int64_t FS, int64_t off, int NX, int NY, int
     const bool xs = side < 2;
     const int n_lines = xs ? NY : NX;
     const int nq = (bathy_only != nullptr) ? 1 : 3 * M;
-    for (int idx = t; idx < n_lines * 2 * nq; idx += NTA) {
+    // BU items per thread per round, all loads before the stores (sources
+    // are interior cells, destinations ghost cells): a long level-1 side
+    // was a chain of dependent load/store pairs
+    constexpr int BU = 4;
+    const int n_items = n_lines * 2 * nq;
+    for (int base = t; base < n_items; base += NTA * BU) {
+        double val[BU];
+        double *dstp[BU];
+#pragma unroll
+        for (int u = 0; u < BU; ++u) {
+            const int idx = base + u * NTA;
+            dstp[u] = nullptr;
+            if (idx >= n_items) continue;
         const int q = idx / (n_lines * 2);
         const int rem = idx - q * n_lines * 2;
         const int line = rem >> 1;
@@ -109,7 +121,12 @@ __device__ void bc_side(double *st, int64_t FS, int64_t off, int NX, int NY, int
             d = off + (int64_t)dst_rc * NX + line;
             s = off + (int64_t)src_rc * NX + line;
         }
-        a[d] = (kind == MLAMR_BC_WALL) ? sign * a[s] : a[s];
+        val[u] = (kind == MLAMR_BC_WALL) ? sign * a[s] : a[s];
+        dstp[u] = a + d;
+        }
+#pragma unroll
+        for (int u = 0; u < BU; ++u)
+            if (dstp[u] != nullptr) *dstp[u] = val[u];
     }
 }
 

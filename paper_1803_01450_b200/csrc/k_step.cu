@@ -93,6 +93,23 @@ __global__ void __launch_bounds__(NTF) k_step_finalize(mlamr_level lv, const dou
     __shared__ bool last;
     const int t = threadIdx.x;
     if (*status != 0) return;
+    // CFL guard (physics.py:342-347) spread over all blocks: a single block
+    // walking every patch was a chain of dependent loads (most of the
+    // launch); violations meet in ticket[1], reset by the last block
+    const double dmin = lv.dx < lv.dy ? lv.dx : lv.dy;
+    {
+        bool v = false;
+        for (int p = blockIdx.x * NTF + t; p < lv.num_patches; p += gridDim.x * NTF) {
+            const long long b = speed_bits[p];
+            if (b < 0) continue;
+            const double sp = __longlong_as_double(b);
+            if ((sp * dt) / dmin > 1.0) {
+                v = true;
+                atomicMin(bad_patch, p);
+            }
+        }
+        if (__any_sync(0xffffffffu, v) && (t & 31) == 0) atomicOr(ticket + 1, 1u);
+    }
     const int K = M + 2;
     const int per = (n_tiles + FIN_BLOCKS - 1) / FIN_BLOCKS;
     const int t0 = blockIdx.x * per, t1 = min(n_tiles, t0 + per);
@@ -115,18 +132,10 @@ __global__ void __launch_bounds__(NTF) k_step_finalize(mlamr_level lv, const dou
         // clipped mass = -(sum of negative depths) * cell area (physics.py:360-362)
         acc[t] = acc[t] + (t < M ? (-sm) * area : sm);
     }
-    if (t == 0) *ticket = 0u;
-    const double dmin = lv.dx < lv.dy ? lv.dx : lv.dy;
-    if (t == 0) viol = 0;
-    __syncthreads();
-    for (int p = t; p < lv.num_patches; p += NTF) {
-        const long long b = speed_bits[p];
-        if (b < 0) continue;
-        const double sp = __longlong_as_double(b);
-        if ((sp * dt) / dmin > 1.0) {
-            atomicOr(&viol, 1);
-            atomicMin(bad_patch, p);
-        }
+    if (t == 0) {
+        viol = (int)((volatile unsigned int *)ticket)[1];
+        ticket[0] = 0u;
+        ticket[1] = 0u;
     }
     __syncthreads();
     if (!viol) return;
@@ -215,8 +224,8 @@ extern "C" int mlamr_step_finalize(mlamr_level lv, const double *src_state, doub
         auto it = pool.find({dev, st});
         if (it == pool.end()) {
             if (cudaMalloc(&sc.chunk, sizeof(double) * FIN_BLOCKS * (MLAMR_MAX_LAYERS + 2)) != cudaSuccess) return -2;
-            if (cudaMalloc(&sc.ticket, sizeof(unsigned int)) != cudaSuccess) return -2;
-            cudaMemsetAsync(sc.ticket, 0, sizeof(unsigned int), st);
+            if (cudaMalloc(&sc.ticket, 2 * sizeof(unsigned int)) != cudaSuccess) return -2;
+            cudaMemsetAsync(sc.ticket, 0, 2 * sizeof(unsigned int), st);
             pool[{dev, st}] = sc;
         } else {
             sc = it->second;
