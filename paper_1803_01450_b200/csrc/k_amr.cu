@@ -733,7 +733,6 @@ __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const doub
                                                       int child_rx, int child_ry, double *patch_mass,
                                                       int32_t *status, const int32_t *plist,
                                                       const int64_t *gbase, const int64_t *plan) {
-    __shared__ double red[NTA];
     __shared__ int bad;
     const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
     const PatchView pv = patch_view(lv, p);
@@ -772,10 +771,25 @@ __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const doub
         }
     }
     if (nonfinite) atomicOr(&bad, 1);
+    // fixed warp-shuffle tree, then the warp partials in warp order (one
+    // barrier instead of a shared-memory tree per layer): deterministic
+    __shared__ double wred[M][NTA / 32];
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-        const double s = block_sum<NTA>(msum[m], red);
-        if (threadIdx.x == 0) patch_mass[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) msum[m] = msum[m] + __shfl_xor_sync(0xffffffffu, msum[m], off);
+    }
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) wred[m][threadIdx.x >> 5] = msum[m];
+    }
+    __syncthreads();
+    if (threadIdx.x < M) {
+        const int m = threadIdx.x;
+        double sm = wred[m][0];
+#pragma unroll
+        for (int w = 1; w < NTA / 32; ++w) sm = sm + wred[m][w];
+        patch_mass[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = sm;
     }
     if (threadIdx.x == 0 && bad) atomicOr(status, MLAMR_ST_NONFINITE);
 }

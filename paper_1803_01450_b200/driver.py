@@ -257,7 +257,9 @@ class Simulation:
         pool = self.levels[level]
         if pool.P == 0:
             return torch.zeros(self.M, dtype=torch.float64, device=self.dev)
-        bpp = pool.blocks_per_patch(pool.max_cells)
+        # a few blocks per patch, each thread over ~8 cells: the per-block
+        # reduction, not the bytes, had dominated with one cell per thread
+        bpp = max(1, min(64, -(-pool.max_cells // (8 * 256))))
         with torch.cuda.stream(self.stream):
             part = self._scratch("reduce", pool.P * bpp * self.M)
             ghosts = pool.state if pool.ghosts_in_cur else pool.other
