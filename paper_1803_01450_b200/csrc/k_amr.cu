@@ -579,24 +579,31 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
     double dsum[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) dsum[m] = 0.0;
+    // old-patch copies (regrid.py:311-323) one fine cell per thread, so a
+    // warp moves contiguous row segments; old patches are ratio-aligned, so
+    // a coarse cell's fine block lies in one old patch and the owner of the
+    // fine cell is the owner the refine pass below tests
+    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nv.nx * nv.ny; idx += gridDim.x * NTA) {
+        const int j = idx / nv.nx, i = idx - (idx / nv.nx) * nv.nx;
+        const int fi = nv.lo_i + i, fj = nv.lo_j + j;
+        const int o = owner_at(ol.own, ol.level_nx, ol.level_ny, fi, fj);
+        if (o < 0) continue;
+        const int32_t *b = ol.box + 4 * o;
+        const int ONX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+        const int64_t ks = ol.offset[o] + (int64_t)(fj - b[1] + MLAMR_G) * ONX + (fi - b[0] + MLAMR_G);
+        const int64_t kd = nv.off + (int64_t)(j + MLAMR_G) * nv.NX + (i + MLAMR_G);
+        double v[3 * M];
+#pragma unroll
+        for (int f = 0; f < 3 * M; ++f) v[f] = ol.state[f * OF + ks];
+#pragma unroll
+        for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + kd] = v[f];
+    }
     for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
         const int J = idx / cnx, I = idx % cnx;
         const int ci = clo_i + I, cj = clo_j + J;
         const int fi0 = ci * r_x, fj0 = cj * r_y;
         const int o = owner_at(ol.own, ol.level_nx, ol.level_ny, fi0, fj0);
-        if (o >= 0) {
-            const int32_t *b = ol.box + 4 * o;
-            const int ONX = b[2] - b[0] + 1 + 2 * MLAMR_G;
-            for (int q = 0; q < r_y; ++q)
-                for (int pp = 0; pp < r_x; ++pp) {
-                    const int fi = fi0 + pp, fj = fj0 + q;
-                    const int64_t ks = ol.offset[o] + (int64_t)(fj - b[1] + MLAMR_G) * ONX + (fi - b[0] + MLAMR_G);
-                    const int64_t kd = nv.off + (int64_t)(fj - nv.lo_j + MLAMR_G) * nv.NX + (fi - nv.lo_i + MLAMR_G);
-#pragma unroll
-                    for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + kd] = ol.state[f * OF + ks];
-                }
-            continue;
-        }
+        if (o >= 0) continue;   // copied above
         Coarse5<M> c;
         gather5<M>(par, par.state, nullptr, 0.0, false, ci, cj, c);
         if (!c.avail[0]) {  // coarse data under the region is incomplete (refine.py:222-225)

@@ -530,7 +530,7 @@ class Simulation:
             if init and fixed is None and self.pb.init_mode == "scenario":
                 self._set_initial(new)
             elif new.P:
-                bpp = new.blocks_per_patch(new.max_interior // (rx * ry))
+                bpp = new.blocks_per_patch(new.max_interior // 4)   # copy pass: ~4 fine cells per thread
                 part = self._scratch("refine", new.P * bpp * M)
                 fs = self.spec(level + 1)
                 ol = old.struct() if old is not None else empty_level_struct(fs, M)

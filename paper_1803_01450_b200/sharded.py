@@ -397,7 +397,7 @@ class ShardedSimulation(Simulation):
             if init and fixed is None and self.pb.init_mode == "scenario":
                 self._set_initial(new)
             elif new.P:
-                bpp = new.blocks_per_patch(new.max_interior // (rx * ry))
+                bpp = new.blocks_per_patch(new.max_interior // 4)   # copy pass: ~4 fine cells per thread
                 part = torch.zeros(new.P * bpp * M, dtype=torch.float64, device=self.dev)
                 ol = old.struct() if old is not None else empty_level_struct(self.spec(level + 1), M)
                 pl, nl = new.work_list()
