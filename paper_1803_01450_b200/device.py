@@ -241,16 +241,9 @@ class LevelPool:
             _p["upload"] += _t3 - _t2
             self.tile_shape = N.step_tile(int((b[:, 2] - b[:, 0] + 1).max()) if self.P else 0, M)
             self.tile_tx = self.tile_shape[1]
-            tl = tile_list(b, self.tile_shape)
-            _p["tile_list"] += _t.perf_counter() - _t3
-            if self.owned is not None and len(tl):
-                tl = tl[self.owned[tl[:, 0]]]
-            self.tiles = tl
-            self.n_tiles = len(tl)
-            self.tiles_d = A.upload(tl, device, stream) if len(tl) else torch.zeros(3, dtype=torch.int32, device=device)
-            _t5 = _t.perf_counter()
-            self.tile_acc = torch.zeros(max(self.n_tiles, 1) * (M + 2), dtype=torch.float64, device=device)
-            _p["tile_acc"] += _t.perf_counter() - _t5
+            # the step work list is built on first use (tiles_d & co. below):
+            # a regrid then enqueues its fill kernels without waiting for it
+            self._tiles = None
             self.owned_d = None
             self.n_owned = self.P
             if self.owned is not None:
@@ -276,6 +269,44 @@ class LevelPool:
             if self.gown is not None:
                 N.check(L.mlamr_paint_owner(self.gown.data_ptr(), spec.nx, spec.ny, self.box_d.data_ptr(),
                                             self.P, GHOST_WIDTH, 1, 1, 1, self.max_cells, sh), "paint gown")
+
+    # -- step work list (built lazily) ------------------------------------------
+    def _build_tiles(self) -> None:
+        import time as _t
+        t0 = _t.perf_counter()
+        tl = tile_list(self.boxes, self.tile_shape)
+        if self.owned is not None and len(tl):
+            tl = tl[self.owned[tl[:, 0]]]
+        with torch.cuda.stream(self.stream):
+            td = arena().upload(tl, self.device, self.stream) if len(tl) else \
+                torch.zeros(3, dtype=torch.int32, device=self.device)
+            acc = torch.zeros(max(len(tl), 1) * (self.M + 2), dtype=torch.float64, device=self.device)
+        self._tiles = (tl, len(tl), td, acc)
+        POOL_PROF["tile_list"] += _t.perf_counter() - t0
+
+    @property
+    def tiles(self) -> np.ndarray:
+        if self._tiles is None:
+            self._build_tiles()
+        return self._tiles[0]
+
+    @property
+    def n_tiles(self) -> int:
+        if self._tiles is None:
+            self._build_tiles()
+        return self._tiles[1]
+
+    @property
+    def tiles_d(self) -> torch.Tensor:
+        if self._tiles is None:
+            self._build_tiles()
+        return self._tiles[2]
+
+    @property
+    def tile_acc(self) -> torch.Tensor:
+        if self._tiles is None:
+            self._build_tiles()
+        return self._tiles[3]
 
     def release(self) -> None:
         """Hand the big buffers back for reuse by a later pool."""
