@@ -53,10 +53,20 @@ template <int M>
 __device__ __forceinline__ double zc_of(const StepSmem<M> &s, int m, int k) {
     return (m == M - 1) ? s.S[3 * M][k] : 0.0;
 }
-template <int M>
+template <int M, bool SW = false>
 __device__ __forceinline__ double zf_of(const StepSmem<M> &s, int m, int k) {
-    return (m == M - 1) ? s.S[3 * M][k] : s.eb[m < M - 1 ? m : 0][k];
+    return (m == M - 1) ? s.S[3 * M][k] : (SW ? s.src : s.eb)[m < M - 1 ? m : 0][k];
 }
+// The second sweep finds its eta_{m+1} planes in `src` and its co-wet flags
+// in `wetcol` (SW): the first sweep's update writes them there, next to the
+// planes its neighbours are still reading (see NEXT in sweep_tile), and the
+// second sweep's sources go to the then free `eb` planes.
+template <int M, bool SW>
+__device__ __forceinline__ double *eb_pl(StepSmem<M> &s, int m) { return SW ? s.src[m] : s.eb[m]; }
+template <int M, bool SW>
+__device__ __forceinline__ double *src_pl(StepSmem<M> &s, int m) { return SW ? s.eb[m] : s.src[m]; }
+template <int M, bool SW>
+__device__ __forceinline__ unsigned char *cowet_pl(StepSmem<M> &s) { return SW ? s.wetcol : s.cowet; }
 
 // Post-processing of one interior cell (physics.py:360-376): clip negative
 // depths, the shear blend (M = 2), the wet-prefix repair and zeroing dry
@@ -172,7 +182,8 @@ __device__ __forceinline__ void post_cell(double (&h)[M], double (&hu)[M], doubl
 // (RUN_BC, all-wet path AW) and returns, block-wide, whether every cell
 // phase A read (RUN_A only) or every cell phase C updated is wet in every
 // layer -- the all-wet decision for what follows.
-template <int M, int DIR, bool FIRST, bool AWA, bool AW, bool RUN_A, bool RUN_BC, bool LAST = false>
+template <int M, int DIR, bool FIRST, bool AWA, bool AW, bool RUN_A, bool RUN_BC, bool LAST = false,
+          bool SW = false, bool NEXT = false>
 __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d, double lam, double yd,
                            const mlamr_params &prm, const double (&rr)[4][4], double &best,
                            double &nacc, PostCtx *post = nullptr) {
@@ -221,7 +232,6 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                 }
             }
             const bool interior = FIRST && r >= 1 && r < ny2 - 1 && c >= 1 && c < nx2 - 1 && (AWA || hs > tol);
-            if (FIRST) s.wetcol[k] = hs > tol;
 #pragma unroll
             for (int m = 0; m < M; ++m) {
                 const bool wet = AWA || h[m] > tol;
@@ -265,7 +275,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     FOR_RECT_BEGIN(lr0, fr1, lc0, fc1)
         const int kl = r * PX + c;
         const int kr = kl + STEP;
-        const bool cop = AW || (s.cowet[kl] && s.cowet[kr]);
+        const unsigned char *CW = cowet_pl<M, SW>(s);
+        const bool cop = AW || (CW[kl] && CW[kr]);
         const double cl = s.cw[kl];
         const double cr = s.cw[kr];
 #pragma unroll
@@ -279,8 +290,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                 hL = hl;
                 hR = hr;
             } else {
-                const double Zl = cop ? zc_of<M>(s, m, kl) : zf_of<M>(s, m, kl);
-                const double Zr = cop ? zc_of<M>(s, m, kr) : zf_of<M>(s, m, kr);
+                const double Zl = cop ? zc_of<M>(s, m, kl) : zf_of<M, SW>(s, m, kl);
+                const double Zr = cop ? zc_of<M>(s, m, kr) : zf_of<M, SW>(s, m, kr);
                 const double Zs = Zl > Zr ? Zl : Zr;
                 hL = (hl + Zl) - Zs;
                 if (hL < 0.0) hL = 0.0;
@@ -307,7 +318,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     const double den = SR - SL;
                     double djump;
                     if ((AW && m < M - 1) || (hL > 0.0 && hR > 0.0))
-                        djump = (hr + zf_of<M>(s, m, kr)) - (hl + zf_of<M>(s, m, kl));
+                        djump = (hr + zf_of<M, SW>(s, m, kr)) - (hl + zf_of<M, SW>(s, m, kl));
                     else
                         djump = hR - hL;
                     const double nh = ((SR * FLh) - (SL * FRh)) + ((SL * SR) * djump);
@@ -331,15 +342,15 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
         const int a = DIR == 0 ? c : r;
         if (M > 1 && a + 1 < n_along - 1) {
             const int k = kr, km = kl, kp = kr + STEP;
-            const bool wm = AW || (s.cowet[km] && s.cowet[k]);
-            const bool wp = AW || (s.cowet[k] && s.cowet[kp]);
+            const bool wm = AW || (CW[km] && CW[k]);
+            const bool wp = AW || (CW[k] && CW[kp]);
 #pragma unroll
             for (int m = 1; m < M; ++m) {
                 double acc = 0.0;
                 bool has = false;
                 bool ok = true;
                 if (m < M - 1) {
-                    const double *f = s.eb[m < M - 1 ? m : 0];
+                    const double *f = eb_pl<M, SW>(s, m < M - 1 ? m : 0);
                     const double dm = wm ? f[k] - f[km] : 0.0;
                     const double dp = wp ? f[kp] - f[k] : 0.0;
                     const double num = ((-g) * s.S[m][k]) * (0.5 * (dp + dm));
@@ -360,7 +371,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     acc = has ? acc + q : q;
                     has = true;
                 }
-                s.src[m - 1][k] = acc;
+                src_pl<M, SW>(s, m - 1)[k] = acc;
             }
         }
     FOR_RECT_END
@@ -371,11 +382,29 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     // their wetness decides (block-wide, with the closing barrier) whether
     // that sweep can take the all-wet path.
     bool wet_out = true;
-    FOR_RECT_BEGIN(ur0, ur1, uc0, uc1)
+    // NEXT: this update also computes the other sweep's per-cell inputs
+    // (its phase A) from the registers -- the updated cells are exactly the
+    // cells that phase reads.  cw and u are not read by this phase and are
+    // stored at once; eta_{m+1} and the co-wet flags go to the planes the
+    // other sweep reads with SW; v, which this phase reads at neighbours,
+    // waits in registers for the closing barrier.
+    constexpr int MAXIT = (NPAD + NT - 1) / NT;
+    double v2s[NEXT ? MAXIT : 1][M];
+    int k2s[NEXT ? MAXIT : 1];
+#pragma unroll
+    for (int it = 0; it < (NEXT ? MAXIT : 1); ++it) k2s[it] = -1;
+    const unsigned char *CWc = cowet_pl<M, SW>(s);
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+        const int idx_ = threadIdx.x + it * NT;
+        if (idx_ >= (ur1 - ur0) * PX) break;
+        const int r = ur0 + idx_ / PX;
+        const int c = idx_ - (idx_ / PX) * PX;
+        if (c < uc0 || c >= uc1) continue;
         const int k = r * PX + c;
         const int km = k - STEP, kp = k + STEP;
-        const bool copl = AW || (s.cowet[km] && s.cowet[k]);
-        const bool copr = AW || (s.cowet[k] && s.cowet[kp]);
+        const bool copl = AW || (CWc[km] && CWc[k]);
+        const bool copr = AW || (CWc[k] && CWc[kp]);
         double nh[M], nn[M], nt[M];   // LAST: the updated cell stays in registers
 #pragma unroll
         for (int m = 0; m < M; ++m) {
@@ -402,10 +431,10 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             } else {
                 // this cell's reconstructed depths at its two faces: hsR of the
                 // left interface and hsL of the right one (physics.py:113-121)
-                const double Zl_l = copl ? zc_of<M>(s, m, km) : zf_of<M>(s, m, km);
-                const double Zk_l = copl ? zc_of<M>(s, m, k) : zf_of<M>(s, m, k);
-                const double Zk_r = copr ? zc_of<M>(s, m, k) : zf_of<M>(s, m, k);
-                const double Zr_r = copr ? zc_of<M>(s, m, kp) : zf_of<M>(s, m, kp);
+                const double Zl_l = copl ? zc_of<M>(s, m, km) : zf_of<M, SW>(s, m, km);
+                const double Zk_l = copl ? zc_of<M>(s, m, k) : zf_of<M, SW>(s, m, k);
+                const double Zk_r = copr ? zc_of<M>(s, m, k) : zf_of<M, SW>(s, m, k);
+                const double Zr_r = copr ? zc_of<M>(s, m, kp) : zf_of<M, SW>(s, m, kp);
                 const double Zs_l = Zl_l > Zk_l ? Zl_l : Zk_l;
                 const double Zs_r = Zk_r > Zr_r ? Zk_r : Zr_r;
                 double hsR_l = (h0 + Zk_l) - Zs_l;
@@ -417,7 +446,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             if (M > 1) {
                 double sm;
                 if (m == 0) {  // physics.py:210, from the pre-sweep eta_1 and own h_0
-                    const double *f = s.eb[0];
+                    const double *f = eb_pl<M, SW>(s, 0);
                     const double dm = copl ? f[k] - f[km] : 0.0;
                     const double dp = copr ? f[kp] - f[k] : 0.0;
                     const double num = ((-g) * h0) * (0.5 * (dp + dm));
@@ -425,7 +454,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     sm = div_fast(num, d, yd, ok);
                     if (!ok) sm = num / d;
                 } else {
-                    sm = s.src[m - 1][k];
+                    sm = src_pl<M, SW>(s, m - 1)[k];
                 }
                 hn = hn + dt * sm;
             }
@@ -442,8 +471,55 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             if (DIR == 0) post_cell<M>(nh, nn, nt, *post, r, c);
             else post_cell<M>(nh, nt, nn, *post, r, c);
         }
-    FOR_RECT_END
-    return __syncthreads_and(wet_out) != 0;
+        if (NEXT) {
+            // the other sweep's phase A (general path) on the updated cell:
+            // its normal momentum is this sweep's transverse one (nt)
+            double hs = 0.0;
+            bool w = true;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                hs = hs + nh[m];
+                w = w && (nh[m] > tol);
+            }
+            s.cw[k] = sqrt(g * np_max(hs, 0.0));
+            cowet_pl<M, !SW>(s)[k] = (M == 1) ? 1 : w;
+            if (M > 1) {
+                double e = B[k];
+#pragma unroll
+                for (int m = M - 1; m >= 1; --m) {
+                    e = e + nh[m];
+                    eb_pl<M, !SW>(s, m - 1)[k] = e;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                double u = 0.0, v = 0.0;
+                if (nh[m] > tol) {
+                    bool ok = true;
+                    const double y = recip_nr(nh[m]);
+                    u = div_fast(nt[m], nh[m], y, ok);
+                    v = div_fast(nn[m], nh[m], y, ok);
+                    if (!ok) {
+                        u = nt[m] / nh[m];
+                        v = nn[m] / nh[m];
+                    }
+                }
+                s.u[m][k] = u;
+                v2s[NEXT ? it : 0][m] = v;
+            }
+            k2s[NEXT ? it : 0] = k;
+        }
+    }
+    const bool all_wet = __syncthreads_and(wet_out) != 0;
+    if (NEXT) {
+#pragma unroll
+        for (int it = 0; it < MAXIT; ++it) {
+            if (k2s[it] < 0) continue;
+#pragma unroll
+            for (int m = 0; m < M; ++m) s.v[m][k2s[it]] = v2s[it][m];
+        }
+    }
+    return all_wet;
 }
 
 
@@ -562,8 +638,11 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const double l1 = YFIRST ? lam_y : lam_x, l2 = YFIRST ? lam_x : lam_y;
     const double q1 = YFIRST ? y_y : y_x, q2 = YFIRST ? y_x : y_y;
     const bool aw1 = sweep_tile<M, D1, true, false, false, true, false>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc);
-    const bool aw2 = aw1 ? sweep_tile<M, D1, true, false, true, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc)
-                         : sweep_tile<M, D1, true, false, false, false, true>(s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc);
+    // the first sweep's update also prepares the second sweep's inputs (NEXT)
+    const bool aw2 = aw1 ? sweep_tile<M, D1, true, false, true, false, true, false, false, true>(
+                               s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc)
+                         : sweep_tile<M, D1, true, false, false, false, true, false, false, true>(
+                               s, ny2, nx2, dt, d1, l1, q1, prm, rr, best, nacc);
     // post-processing on the tile interior (physics.py:360-376), fused into
     // the second sweep's update of exactly those cells
     PostCtx pc;
@@ -577,9 +656,9 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     for (int m = 0; m < MLAMR_MAX_LAYERS; ++m) pc.negs[m] = 0.0;
     pc.fixes = pc.repairs = 0;
     if (aw2)
-        sweep_tile<M, D2, false, true, true, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, nacc, &pc);
+        sweep_tile<M, D2, false, true, true, false, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, nacc, &pc);
     else
-        sweep_tile<M, D2, false, false, false, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, nacc, &pc);
+        sweep_tile<M, D2, false, false, false, false, true, true, true>(s, ny2, nx2, dt, d2, l2, q2, prm, rr, best, nacc, &pc);
 
     // per-tile partials in one fused pass: warp shuffles (fixed xor tree),
     // then warp 0 combines the NT/32 warp values in warp order -- the same
