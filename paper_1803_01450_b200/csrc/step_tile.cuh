@@ -624,8 +624,10 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const double lam_x = kc.lam_x, lam_y = kc.lam_y;
     const double y_x = recip_nr(lv.dx), y_y = recip_nr(lv.dy);
     asm volatile("cp.async.wait_group 0;\n" ::);
-    __syncthreads();
-
+    // no barrier here: the first sweep's phase A walks the padded tile with
+    // the staging's own thread -> cell mapping (idx = t + i*NT), so every
+    // thread reads only cells whose copies it issued and has waited for;
+    // phase A's closing barrier publishes the tile to the other threads
     double best = -1.0;  // running observed speed over this thread's cells
     double nacc = 0.0;   // NaN iff a speed operand was NaN
     // each sweep takes the all-wet path when every cell it reads is wet in
