@@ -510,7 +510,9 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
             k2s[NEXT ? it : 0] = k;
         }
     }
-    const bool all_wet = __syncthreads_and(wet_out) != 0;
+    // the last sweep's wetness is not used and nothing reads its shared
+    // planes afterwards (the tile's reductions have their own barrier)
+    const bool all_wet = LAST ? true : (__syncthreads_and(wet_out) != 0);
     if (NEXT) {
 #pragma unroll
         for (int it = 0; it < MAXIT; ++it) {
