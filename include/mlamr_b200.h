@@ -34,6 +34,7 @@ extern "C" {
 #define MLAMR_ST_CFL 1        /* CflViolationError  (physics.py:342-347) */
 #define MLAMR_ST_GEOMETRY 2   /* GeometryError      (refine.py:210-225)  */
 #define MLAMR_ST_NONFINITE 4  /* NumericalAbortError (driver.py:286-297) */
+#define MLAMR_ST_BATHY 8      /* AssertionError: bathymetry does not telescope (coarsen.py:79-100) */
 
 /* boundary kinds, per side in the order left, right, bottom, top */
 #define MLAMR_BC_WALL 0
@@ -208,6 +209,16 @@ int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x, int r_y,
 int mlamr_average_down_flat(mlamr_level fine, mlamr_level coarse, int r_x, int r_y, mlamr_params prm,
                             const int64_t *coarse_base, int64_t n_coarse, const int32_t *status,
                             void *stream);
+
+/* check_bathymetry_consistency (coarsen.py:79-100) for every patch of a new
+ * fine level against the coarse level's interiors: block_mean of the fine
+ * bathymetry (the reference's numpy order, r <= 4) vs the coarse value,
+ * |diff| > atol sets MLAMR_ST_BATHY and the smallest offending fine patch
+ * index in *bad_patch.  `coarse_base` = prefix sums of the coarse cells
+ * under each fine patch (as mlamr_average_down_flat). */
+int mlamr_check_bathymetry(mlamr_level fine, mlamr_level coarse, int r_x, int r_y, double atol,
+                           const int64_t *coarse_base, int64_t n_coarse, int32_t *status,
+                           int32_t *bad_patch, void *stream);
 
 /* ---- K3 + K5: regrid data movement (regrid.py:270-353) -------------------
  * Every new-patch interior cell is copied from the old patch covering it

@@ -217,6 +217,40 @@ class OPatch:
         return self.sl(self.box)
 
 
+class BoxIndex:
+    """Bucket grid over a patch list, keyed by every patch's frame (box grown
+    by the ghost width).  ``query(box)`` returns, in list order, the patches
+    whose frame meets ``box``: a superset of every interior or frame overlap
+    the reference's O(P) scans find (ghost.py:58-84, :186-196; regrid.py:311-323,
+    :334-348; coarsen.py:46-75, :79-100).  The scans below then run unchanged
+    over the candidates, so their order and arithmetic are the reference's;
+    the index only skips patches that cannot meet the box (test
+    infrastructure: it makes the oracle reach the BASELINE sizes)."""
+
+    S = 16
+
+    def __init__(self, patches):
+        self.patches = patches
+        self.n = len(patches)
+        self.buckets = {}
+        S = self.S
+        for k, p in enumerate(patches):
+            f = p.box.grow(GHOST)
+            for bj in range(f.lo_j // S, f.hi_j // S + 1):
+                for bi in range(f.lo_i // S, f.hi_i // S + 1):
+                    self.buckets.setdefault((bj, bi), []).append(k)
+
+    def query(self, box: "Box"):
+        S = self.S
+        ks = set()
+        for bj in range(box.lo_j // S, box.hi_j // S + 1):
+            for bi in range(box.lo_i // S, box.hi_i // S + 1):
+                got = self.buckets.get((bj, bi))
+                if got:
+                    ks.update(got)
+        return [self.patches[k] for k in sorted(ks)]
+
+
 # --------------------------------------------------------------------------
 # physics (physics.py:261-386)
 # --------------------------------------------------------------------------
@@ -278,9 +312,14 @@ class Coarse:
     avail: np.ndarray
 
 
-def gather(patches, box: Box, M: int, blend=None, include_ghosts: bool = True) -> Coarse:
+def gather(patches, box: Box, M: int, blend=None, include_ghosts: bool = True,
+           index: Optional[BoxIndex] = None) -> Coarse:
     """ghost.gather (ghost.py:29-86): interiors first; then, as a fallback,
-    ghost frames in list order with the first provider winning."""
+    ghost frames in list order with the first provider winning.  ``index``
+    (a BoxIndex over ``patches``) restricts both passes to the patches whose
+    frame meets ``box``, in list order."""
+    if index is not None:
+        patches = index.query(box)
     shp = (box.ny, box.nx)
     out = Coarse(box, np.zeros((M,) + shp), np.zeros((M,) + shp), np.zeros((M,) + shp),
                  np.zeros(shp), np.zeros(shp, dtype=bool))
@@ -394,15 +433,19 @@ def block_mean(a: np.ndarray, rx: int, ry: int) -> np.ndarray:
     return out.reshape(lead + (ny // ry, nx // rx))
 
 
-def average_down(fine, coarse, rx: int, ry: int, prm: Params, check_time: bool = True):
-    """coarsen.average_down (coarsen.py:30-76)."""
+def average_down(fine, coarse, rx: int, ry: int, prm: Params, check_time: bool = True,
+                 index: Optional[BoxIndex] = None):
+    """coarsen.average_down (coarsen.py:30-76); ``index`` over ``coarse``."""
     if not fine or not coarse:
         return np.zeros(prm.M)
     if check_time:
+        # every (fine, coarse) pair of the reference's double loop, over the
+        # distinct clocks only (the same test, O(P) instead of O(P^2))
+        ctimes = list(dict.fromkeys(cp.time for cp in coarse))
         for fp in fine:
-            for cp in coarse:
-                if abs(fp.time - cp.time) > 1e-12 * max(1.0, abs(cp.time)):
-                    raise TimeSyncFault(f"level {fp.level} t={fp.time!r} vs {cp.time!r}")
+            for ct in ctimes:
+                if abs(fp.time - ct) > 1e-12 * max(1.0, abs(ct)):
+                    raise TimeSyncFault(f"level {fp.level} t={fp.time!r} vs {ct!r}")
     delta = np.zeros(prm.M)
     for fp in fine:
         cb = fp.box.coarse(rx, ry)
@@ -411,7 +454,7 @@ def average_down(fine, coarse, rx: int, ry: int, prm: Params, check_time: bool =
         dry = avg[0] <= prm.tol
         avg[1][dry] = 0.0
         avg[2][dry] = 0.0
-        for cp in coarse:
+        for cp in (coarse if index is None else index.query(cb)):
             ov = cb.meet(cp.box)
             if ov is None:
                 continue
@@ -709,9 +752,12 @@ def _coverage(boxes, spec: Spec, rx: int, ry: int, coarse_given: bool = False):
     return cov
 
 
-def check_bathymetry_consistency(fp: OPatch, coarse, rx: int, ry: int, atol: float = 1e-12):
+def check_bathymetry_consistency(fp: OPatch, coarse, rx: int, ry: int, atol: float = 1e-12,
+                                 index: Optional[BoxIndex] = None):
     """coarsen.check_bathymetry_consistency (coarsen.py:79-100)."""
     cb = fp.box.coarse(rx, ry)
+    if index is not None:
+        coarse = index.query(cb)
     jj, ii = fp.inner
     avg = block_mean(fp.bathy[jj, ii], rx, ry)
     for cp in coarse:
@@ -788,6 +834,17 @@ class Simulation:
     def spec(self, level: int) -> Spec:
         return self.specs[level - 1]
 
+    def _index(self, level: int) -> BoxIndex:
+        """BoxIndex over the level's current patch list (rebuilt when a
+        regrid replaces the list)."""
+        cache = self.__dict__.setdefault("_idx", {})
+        ix = cache.get(level)
+        pats = self.patches[level]
+        if ix is None or ix.patches is not pats or ix.n != len(pats):
+            ix = BoxIndex(pats)
+            cache[level] = ix
+        return ix
+
     def level_box(self, level: int) -> Box:
         s = self.spec(level)
         return Box(0, 0, s.nx - 1, s.ny - 1)
@@ -831,14 +888,17 @@ class Simulation:
             theta = min(1.0, max(0.0, (t - t0) / dt)) if dt > 0 else 1.0
             blend = (theta, old)
         M = self.prm.M
-        return lambda box: gather(parents, box, M, blend=blend)
+        index = self._index(level - 1)
+        return lambda box: gather(parents, box, M, blend=blend, index=index)
 
     def fill_level_ghosts(self, level: int, t: float) -> None:
         ps = self.spec(level - 1) if level > 1 else None
         prov = self._provider(level, t)
         sib = self.patches[level]
+        index = self._index(level)
         for p in sib:
-            fill_ghosts(p, sib, prov, self.pb.boundaries, self.level_box(level),
+            # the siblings whose interior can meet p's frame, in list order
+            fill_ghosts(p, index.query(p.full), prov, self.pb.boundaries, self.level_box(level),
                         ps.r_x if ps else 1, ps.r_y if ps else 1, self.prm)
 
     # -- regridding (driver.py:192-222, regrid.py:235-353) ------------------
@@ -889,6 +949,7 @@ class Simulation:
         if sorted(nboxes, key=key) == sorted((p.box for p in old), key=key):
             return False
         old_cov = _coverage([p.box for p in old], s, rx, ry)
+        old_index = BoxIndex(old)
         carea = s.dx * s.dy
         M = self.prm.M
         rdelta = np.zeros(M)
@@ -896,16 +957,17 @@ class Simulation:
         for fb, cb in zip(nboxes, cboxes):
             p = self._new_patch(level + 1, fb)
             p.time = sync_time
-            check_bathymetry_consistency(p, self.patches[level], rx, ry)
+            check_bathymetry_consistency(p, self.patches[level], rx, ry, index=self._index(level))
             if init and fixed is None and self.pb.init_mode == "scenario":
                 self._init_from_problem(p)
             else:
                 mask = ~old_cov[cb.lo_j:cb.hi_j + 1, cb.lo_i:cb.hi_i + 1]
                 for run in row_runs(mask, cb):
-                    c = gather(self.patches[level], run.grow(1), M, include_ghosts=False)
+                    c = gather(self.patches[level], run.grow(1), M, include_ghosts=False,
+                               index=self._index(level))
                     rdelta += refine_patch(c, p, rx, ry, self.prm, region=run.fine(rx, ry),
                                            coarse_cell_area=carea)
-                for o in old:
+                for o in old_index.query(fb):
                     ov = fb.meet(o.box)
                     if ov is None:
                         continue
@@ -929,7 +991,7 @@ class Simulation:
                 jj, ii = o.inner
                 fmass = (o.h[:, jj, ii] * fmask[None]).sum(axis=(1, 2)) * (fs.dx * fs.dy)
                 cv = np.zeros(M)
-                for cp in self.patches[level]:
+                for cp in self._index(level).query(cb):
                     ov = cb.meet(cp.box)
                     if ov is None:
                         continue
@@ -995,7 +1057,7 @@ class Simulation:
                 self.advance_level(level + 1, dtf, t0 + k * dtf)
             for p in self.patches[level + 1]:
                 p.time = t1
-            average_down(self.patches[level + 1], pats, s.r_x, s.r_y, self.prm)
+            average_down(self.patches[level + 1], pats, s.r_x, s.r_y, self.prm, index=self._index(level))
             del self._stash[level]
 
     def check_finite(self) -> None:

@@ -16,6 +16,7 @@ MAX_LAYERS = 4
 ST_CFL = 1
 ST_GEOMETRY = 2
 ST_NONFINITE = 4
+ST_BATHY = 8
 BC_KIND = {"wall": 0, "outflow": 1}
 SIDES = ("left", "right", "bottom", "top")
 
@@ -114,6 +115,8 @@ SIGNATURES = {
     "mlamr_copy_pairs_of_plan": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp,
                                                 c_vp]),
     "mlamr_fill_copy_pairs": (ctypes.c_int, [c_vp, ctypes.c_int64, c_vp, ctypes.c_int64, ctypes.c_int, c_vp, c_vp]),
+    "mlamr_check_bathymetry": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, ctypes.c_double, c_vp,
+                                              ctypes.c_int64, c_vp, c_vp, c_vp]),
     "mlamr_average_down_flat": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, Params, c_vp,
                                                ctypes.c_int64, c_vp, c_vp]),
     "mlamr_pt_create": (ctypes.c_void_p, [Params, c_vp, c_vp]),

@@ -27,16 +27,8 @@ from dataclasses import dataclass, fields
 
 import numpy as np
 
-from .errors import MlamrError
+from .errors import ConfigError, MlamrError  # noqa: F401  (ConfigError re-exported)
 from .problems import Problem
-
-
-class ConfigError(MlamrError):
-    """Invalid or unknown configuration input; carries the offending key path."""
-
-    def __init__(self, key: str, message: str):
-        self.key = key
-        super().__init__(f"{key}: {message}")
 
 
 def _floats(text: str) -> tuple:

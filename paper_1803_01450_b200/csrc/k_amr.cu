@@ -20,8 +20,9 @@ constexpr int NTA = 256;
 // owner maps
 // ---------------------------------------------------------------------------
 __global__ void k_paint(int32_t *map, int map_nx, int map_ny, const int32_t *box, int grow,
-                        int first_wins, int r_x, int r_y) {
-    const int p = blockIdx.y;
+                        int first_wins, int r_x, int r_y, int nrows) {
+    const int p = grid_row();
+    if (p >= nrows) return;
     const int32_t *b = box + 4 * p;
     int lo_i = b[0], lo_j = b[1], hi_i = b[2], hi_j = b[3];
     if (r_x > 1 || r_y > 1) {  // coarsened footprint (aligned boxes)
@@ -199,7 +200,8 @@ __global__ void __launch_bounds__(NTA) k_fill_ghosts(mlamr_level lv, mlamr_level
 // (physical BC, ghost.py:132-142).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(NTA) k_ghost_plan(mlamr_level lv, const int64_t *gbase, int64_t *plan) {
-    const int p = blockIdx.y;
+    const int p = grid_row();
+    if (p >= lv.num_patches) return;
     const PatchView pv = patch_view(lv, p);
     const int nghost = 4 * pv.NX + 4 * pv.ny;
     for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nghost; idx += gridDim.x * NTA) {
@@ -336,11 +338,13 @@ __global__ void __launch_bounds__(NTA) k_fill_copy_pairs(double *__restrict__ st
 // the listed patches writes its pair, or (-1, -1) when it has no sibling
 __global__ void __launch_bounds__(NTA) k_copy_pairs_of_plan(mlamr_level lv, const int64_t *gbase,
                                                             const int64_t *plan, const int32_t *plist,
-                                                            const int64_t *pbase, int64_t *pairs) {
-    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+                                                            const int64_t *pbase, int64_t *pairs, int nrows) {
+    const int row = grid_row();
+    if (row >= nrows) return;
+    const int p = plist ? plist[row] : row;
     const PatchView pv = patch_view(lv, p);
     const int nghost = 4 * pv.NX + 4 * pv.ny;
-    const int64_t out0 = pbase[blockIdx.y];
+    const int64_t out0 = pbase[row];
     for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nghost; idx += gridDim.x * NTA) {
         const int64_t src = plan[gbase[p] + idx];
         int J, I;
@@ -497,7 +501,8 @@ __global__ void __launch_bounds__(NTA) k_average_down(mlamr_level fine, mlamr_le
     if (status != nullptr && *status != 0) return;
     const int r_x = RX > 0 ? RX : r_x_;
     const int r_y = RY > 0 ? RY : r_y_;
-    const int p = blockIdx.y;
+    const int p = grid_row();
+    if (p >= fine.num_patches) return;
     const PatchView fv = patch_view(fine, p);
     const int cnx = fv.nx / r_x, cny = fv.ny / r_y;
     const int clo_i = floordiv(fv.lo_i, r_x), clo_j = floordiv(fv.lo_j, r_y);
@@ -558,6 +563,46 @@ __global__ void __launch_bounds__(NTA) k_average_down_flat(mlamr_level fine, mla
     }
 }
 
+// check_bathymetry_consistency (coarsen.py:79-100): one thread per coarse
+// cell under a new fine patch (flat list, as k_average_down_flat); the fine
+// block mean in the reference's numpy order against the coarse interior
+// value, atol absolute.
+__global__ void __launch_bounds__(NTA) k_check_bathy(mlamr_level fine, mlamr_level coarse, int r_x, int r_y,
+                                                     double atol, const int64_t *__restrict__ cbase,
+                                                     int64_t n_coarse, int32_t *status, int32_t *bad) {
+    const double nblk = (double)(r_x * r_y);
+    for (int64_t c = (int64_t)blockIdx.x * NTA + threadIdx.x; c < n_coarse; c += (int64_t)gridDim.x * NTA) {
+        int lo = 0, hi = fine.num_patches - 1;   // last p with cbase[p] <= c
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (cbase[mid] <= c) lo = mid; else hi = mid - 1;
+        }
+        const int p = lo;
+        const PatchView fv = patch_view(fine, p);
+        const int cnx = fv.nx / r_x;
+        const int idx = (int)(c - cbase[p]);
+        const int J = idx / cnx, I = idx - (idx / cnx) * cnx;
+        const int ci = floordiv(fv.lo_i, r_x) + I, cj = floordiv(fv.lo_j, r_y) + J;
+        const int o = owner_at(coarse.own, coarse.level_nx, coarse.level_ny, ci, cj);
+        if (o < 0) continue;
+        const double *a = fine.bathy + fv.off + (int64_t)(MLAMR_G + J * r_y) * fv.NX + (MLAMR_G + I * r_x);
+        double s = 0.0;
+        for (int q = 0; q < r_y; ++q) {
+            double rs = a[(int64_t)q * fv.NX];
+            for (int pp = 1; pp < r_x; ++pp) rs = rs + a[(int64_t)q * fv.NX + pp];
+            s = (q == 0) ? rs : s + rs;
+        }
+        const double mean = s / nblk;
+        const int32_t *b = coarse.box + 4 * o;
+        const int CNX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+        const double cv = coarse.bathy[coarse.offset[o] + (int64_t)(cj - b[1] + MLAMR_G) * CNX + (ci - b[0] + MLAMR_G)];
+        if (fabs(mean - cv) > atol) {
+            atomicOr(status, MLAMR_ST_BATHY);
+            atomicMin(bad, p);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K3 + K5: regrid data movement (regrid.rebuild_child_level, regrid.py:270-353)
 // One thread per coarse cell of a new patch's footprint: either copy its
@@ -567,9 +612,12 @@ __global__ void __launch_bounds__(NTA) k_average_down_flat(mlamr_level fine, mla
 template <int M>
 __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
                                                      int r_x, int r_y, mlamr_params prm,
-                                                     double *refine_delta, int32_t *status, const int32_t *plist) {
+                                                     double *refine_delta, int32_t *status, const int32_t *plist,
+                                                     int nrows) {
     __shared__ double red[NTA];
-    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+    const int row = grid_row();
+    if (row >= nrows) return;
+    const int p = plist ? plist[row] : row;
     const PatchView nv = patch_view(nl, p);
     const int cnx = nv.nx / r_x, cny = nv.ny / r_y;
     const int clo_i = floordiv(nv.lo_i, r_x), clo_j = floordiv(nv.lo_j, r_y);
@@ -643,9 +691,12 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
 // but by no new one: coarse mass minus the discarded fine mass.
 template <int M>
 __global__ void __launch_bounds__(NTA) k_derefine(mlamr_level ol, mlamr_level par, const int32_t *new_child,
-                                                  int r_x, int r_y, double *delta, const int32_t *plist) {
+                                                  int r_x, int r_y, double *delta, const int32_t *plist,
+                                                  int nrows) {
     __shared__ double red[NTA];
-    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+    const int row = grid_row();
+    if (row >= nrows) return;
+    const int p = plist ? plist[row] : row;
     const PatchView ov = patch_view(ol, p);
     const int cnx = ov.nx / r_x, cny = ov.ny / r_y;
     const int clo_i = floordiv(ov.lo_i, r_x), clo_j = floordiv(ov.lo_j, r_y);
@@ -739,9 +790,11 @@ __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const doub
                                                       const double *ghosts, const int32_t *child,
                                                       int child_rx, int child_ry, double *patch_mass,
                                                       int32_t *status, const int32_t *plist,
-                                                      const int64_t *gbase, const int64_t *plan) {
+                                                      const int64_t *gbase, const int64_t *plan, int nrows) {
     __shared__ int bad;
-    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+    const int row = grid_row();
+    if (row >= nrows) return;
+    const int p = plist ? plist[row] : row;
     const PatchView pv = patch_view(lv, p);
     const int64_t FS = lv.field_stride;
     if (threadIdx.x == 0) bad = 0;
@@ -808,8 +861,10 @@ __global__ void __launch_bounds__(NTA) k_level_reduce(mlamr_level lv, const doub
 template <int M>
 __global__ void __launch_bounds__(NTA) k_flag_cells(mlamr_level lv, const double *st, mlamr_params prm,
                                                     const double *eta_rest, const double *wave_tol,
-                                                    uint8_t *bits, const int32_t *plist) {
-    const int p = plist ? plist[blockIdx.y] : (int)blockIdx.y;
+                                                    uint8_t *bits, const int32_t *plist, int nrows) {
+    const int row = grid_row();
+    if (row >= nrows) return;
+    const int p = plist ? plist[row] : row;
     const PatchView pv = patch_view(lv, p);
     const int64_t FS = lv.field_stride;
     const double tol = prm.dry_tolerance;
@@ -931,8 +986,8 @@ extern "C" int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int
                                  int num_patches, int grow, int first_wins, int r_x, int r_y,
                                  int max_cells, void *stream) {
     if (num_patches <= 0) return 0;
-    dim3 grid(blocks_for(max_cells, 256), num_patches);
-    k_paint<<<grid, NTA, 0, as_stream(stream)>>>(map, map_nx, map_ny, box, grow, first_wins, r_x, r_y);
+    const dim3 grid = row_grid(blocks_for(max_cells, 256), num_patches);
+    k_paint<<<grid, NTA, 0, as_stream(stream)>>>(map, map_nx, map_ny, box, grow, first_wins, r_x, r_y, num_patches);
     return (int)cudaGetLastError();
 }
 
@@ -956,7 +1011,7 @@ extern "C" int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent, cons
 extern "C" int mlamr_ghost_plan(mlamr_level lv, const int64_t *gbase, int64_t *plan, int max_ghost,
                                 void *stream) {
     if (lv.num_patches <= 0) return 0;
-    dim3 grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), (unsigned)lv.num_patches);
+    const dim3 grid = row_grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), lv.num_patches);
     k_ghost_plan<<<grid, NTA, 0, as_stream(stream)>>>(lv, gbase, plan);
     return (int)cudaGetLastError();
 }
@@ -989,8 +1044,8 @@ extern "C" int mlamr_copy_pairs_of_plan(mlamr_level lv, const int64_t *gbase, co
                                         int max_ghost, int64_t *pairs, void *stream) {
     const int nb = patch_list ? n_list : lv.num_patches;
     if (nb <= 0) return 0;
-    dim3 grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), (unsigned)nb);
-    k_copy_pairs_of_plan<<<grid, NTA, 0, as_stream(stream)>>>(lv, gbase, plan, patch_list, list_base, pairs);
+    const dim3 grid = row_grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), nb);
+    k_copy_pairs_of_plan<<<grid, NTA, 0, as_stream(stream)>>>(lv, gbase, plan, patch_list, list_base, pairs, nb);
     return (int)cudaGetLastError();
 }
 
@@ -1019,7 +1074,7 @@ extern "C" int mlamr_average_down(mlamr_level fine, mlamr_level coarse, int r_x,
                                   double *patch_delta, int blocks_per_patch, const int32_t *status,
                                   void *stream) {
     if (fine.num_patches <= 0) return 0;
-    dim3 grid(blocks_per_patch, fine.num_patches);
+    const dim3 grid = row_grid(blocks_per_patch, fine.num_patches);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
@@ -1057,17 +1112,27 @@ extern "C" int mlamr_average_down_flat(mlamr_level fine, mlamr_level coarse, int
     return (int)cudaGetLastError();
 }
 
+extern "C" int mlamr_check_bathymetry(mlamr_level fine, mlamr_level coarse, int r_x, int r_y, double atol,
+                                      const int64_t *coarse_base, int64_t n_coarse, int32_t *status,
+                                      int32_t *bad_patch, void *stream) {
+    if (fine.num_patches <= 0 || n_coarse <= 0 || coarse.num_patches <= 0) return 0;
+    const int blocks = (int)std::min<int64_t>((n_coarse + NTA - 1) / NTA, 148 * 8);
+    k_check_bathy<<<blocks, NTA, 0, as_stream(stream)>>>(fine, coarse, r_x, r_y, atol, coarse_base, n_coarse, status,
+                                                         bad_patch);
+    return (int)cudaGetLastError();
+}
+
 extern "C" int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_level parent, int r_x, int r_y,
                                  mlamr_params prm, double *refine_delta, int blocks_per_patch,
                                  int32_t *status, const int32_t *patch_list, int n_list, void *stream) {
     const int nb = patch_list ? n_list : newlv.num_patches;
     if (nb <= 0) return 0;
-    dim3 grid(blocks_per_patch, nb);
+    const dim3 grid = row_grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
         k_regrid_fill<M><<<grid, NTA, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status,
-                                               patch_list);
+                                               patch_list, nb);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -1078,11 +1143,11 @@ extern "C" int mlamr_derefine_delta(mlamr_level oldlv, mlamr_level parent, const
                                     int blocks_per_patch, const int32_t *patch_list, int n_list, void *stream) {
     const int nb = patch_list ? n_list : oldlv.num_patches;
     if (nb <= 0) return 0;
-    dim3 grid(blocks_per_patch, nb);
+    const dim3 grid = row_grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta, patch_list);
+        k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta, patch_list, nb);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -1120,13 +1185,13 @@ extern "C" int mlamr_level_reduce_planned(mlamr_level lv, const double *interior
                                           void *stream) {
     const int nb = patch_list ? n_list : lv.num_patches;
     if (nb <= 0) return 0;
-    dim3 grid(blocks_per_patch, nb);
+    const dim3 grid = row_grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(lv.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
         k_level_reduce<M><<<grid, NTA, 0, st>>>(lv, interior_state, ghost_state, child, 1, 1, patch_mass,
                                                 status, patch_list, ghost_plan ? ghost_base : nullptr,
-                                                ghost_plan);
+                                                ghost_plan, nb);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -1137,11 +1202,11 @@ extern "C" int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_param
                                 const int32_t *patch_list, int n_list, void *stream) {
     const int nb = patch_list ? n_list : lv.num_patches;
     if (nb <= 0) return 0;
-    dim3 grid(blocks_per_patch, nb);
+    const dim3 grid = row_grid(blocks_per_patch, nb);
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_flag_cells<M><<<grid, NTA, 0, st>>>(lv, state, prm, eta_rest, wave_tol, cell_bits, patch_list);
+        k_flag_cells<M><<<grid, NTA, 0, st>>>(lv, state, prm, eta_rest, wave_tol, cell_bits, patch_list, nb);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -1151,8 +1216,9 @@ extern "C" int mlamr_flag_cells(mlamr_level lv, const double *state, mlamr_param
 // another pool): seg[3*s] = src offset, seg[3*s+1] = dst offset, seg[3*s+2]
 // = length in elements, applied to every one of `nplanes` planes.
 __global__ void k_copy_segments(const double *__restrict__ src, int64_t src_stride, double *__restrict__ dst,
-                                int64_t dst_stride, const int64_t *__restrict__ seg, int nplanes) {
-    const int sg = blockIdx.y;
+                                int64_t dst_stride, const int64_t *__restrict__ seg, int nplanes, int nrows) {
+    const int sg = grid_row();
+    if (sg >= nrows) return;
     const int64_t so = seg[3 * sg], doff = seg[3 * sg + 1], len = seg[3 * sg + 2];
     for (int q = 0; q < nplanes; ++q)
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
@@ -1164,8 +1230,9 @@ extern "C" int mlamr_copy_segments(const double *src, int64_t src_stride, double
                                    const int64_t *segments, int n_segments, int max_len, int nplanes,
                                    void *stream) {
     if (n_segments <= 0) return 0;
-    dim3 grid((unsigned)std::max(1, std::min(8, (max_len + 255) / 256)), (unsigned)n_segments);
-    k_copy_segments<<<grid, 256, 0, as_stream(stream)>>>(src, src_stride, dst, dst_stride, segments, nplanes);
+    const dim3 grid = row_grid((unsigned)std::max(1, std::min(8, (max_len + 255) / 256)), n_segments);
+    k_copy_segments<<<grid, 256, 0, as_stream(stream)>>>(src, src_stride, dst, dst_stride, segments, nplanes,
+                                                         n_segments);
     return (int)cudaGetLastError();
 }
 
@@ -1177,7 +1244,8 @@ extern "C" int mlamr_copy_segments(const double *src, int64_t src_stride, double
 __global__ void __launch_bounds__(NTA) k_pack_interiors(mlamr_level lv, double *state, double *packed,
                                                         const int64_t *pbase, int64_t ntot, int nplanes,
                                                         int unpack) {
-    const int p = blockIdx.y;
+    const int p = grid_row();
+    if (p >= lv.num_patches) return;
     const PatchView pv = patch_view(lv, p);
     const int n = pv.nx * pv.ny;
     const int64_t pb = pbase[p];
@@ -1197,7 +1265,7 @@ __global__ void __launch_bounds__(NTA) k_pack_interiors(mlamr_level lv, double *
 extern "C" int mlamr_pack_interiors(mlamr_level lv, double *state, double *packed, const int64_t *pbase,
                                     int64_t n_total, int max_interior, int unpack, void *stream) {
     if (lv.num_patches <= 0) return 0;
-    dim3 grid((unsigned)std::max(1, std::min(4, (max_interior + NTA - 1) / NTA)), (unsigned)lv.num_patches);
+    const dim3 grid = row_grid((unsigned)std::max(1, std::min(4, (max_interior + NTA - 1) / NTA)), lv.num_patches);
     k_pack_interiors<<<grid, NTA, 0, as_stream(stream)>>>(lv, state, packed, pbase, n_total, 3 * lv.num_layers,
                                                           unpack);
     return (int)cudaGetLastError();
@@ -1313,8 +1381,10 @@ extern "C" int mlamr_sat_u8(const uint8_t *map, int ny, int nx, int invert, int3
 // patch_list (optional) selects the patches, e.g. a rank's owned ones.
 __global__ void k_pack_frame(mlamr_level lv, const double *__restrict__ state, int level_index,
                              const int64_t *__restrict__ rec_off, const int32_t *__restrict__ patch_list,
-                             double *__restrict__ out) {
-    const int p = patch_list ? patch_list[blockIdx.y] : blockIdx.y;
+                             double *__restrict__ out, int nrows) {
+    const int row = grid_row();
+    if (row >= nrows) return;
+    const int p = patch_list ? patch_list[row] : row;
     const PatchView pv = patch_view(lv, p);
     const int M = lv.num_layers;
     const int64_t n = (int64_t)pv.nx * pv.ny;
@@ -1342,8 +1412,8 @@ extern "C" int mlamr_pack_frame(mlamr_level lv, const double *state, int level_i
                                 void *stream) {
     const int np = patch_list ? n_list : lv.num_patches;
     if (np <= 0) return 0;
-    dim3 grid(blocks_per_patch > 0 ? blocks_per_patch : 1, np);
-    k_pack_frame<<<grid, NTA, 0, as_stream(stream)>>>(lv, state, level_index, rec_off, patch_list, out);
+    const dim3 grid = row_grid(blocks_per_patch > 0 ? blocks_per_patch : 1, np);
+    k_pack_frame<<<grid, NTA, 0, as_stream(stream)>>>(lv, state, level_index, rec_off, patch_list, out, np);
     return (int)cudaGetLastError();
 }
 

@@ -25,6 +25,7 @@ composite mass) plus once per regrid (flag map).
 
 from __future__ import annotations
 
+import copy
 import ctypes
 import os
 import time
@@ -126,6 +127,7 @@ class Simulation:
                 self._rebuild(lev, init=True)
             self._mass_prev = self.composite_mass()
             self.stats.initial_mass = list(self._mass_prev)
+            self._sync_status("building the initial hierarchy")
         if reserve_factor > 0:
             from .device import reserve
             reserve(int(reserve_factor * self.device_bytes()), self.dev, self.stream)
@@ -222,7 +224,20 @@ class Simulation:
         if pool.P:
             self._call(self.lib.mlamr_fill_bathymetry, pool.struct(), self.level_bathy[level - 1].data_ptr(),
                        self.bcs, self.sh)
+            if level > 1 and level - 1 in self.levels:
+                self._check_bathymetry(pool, self.levels[level - 1], self.spec(level - 1))
         return pool
+
+    def _check_bathymetry(self, fine: LevelPool, coarse: LevelPool, cs: LevelSpec) -> None:
+        """check_bathymetry_consistency (coarsen.py:79-100) for every new
+        fine patch against the coarse interiors, on the device; a violation
+        sets MLAMR_ST_BATHY, raised as the reference's AssertionError at the
+        next status check (the end of this coarse step, or construction)."""
+        if coarse.P == 0:
+            return
+        cbase, n = fine.coarse_base(cs.r_x, cs.r_y)
+        self._call(self.lib.mlamr_check_bathymetry, fine.struct(), coarse.struct(), cs.r_x, cs.r_y, 1e-12,
+                   cbase.data_ptr(), n, self.status.data_ptr(), self.bad.data_ptr(), self.sh)
 
     def _set_initial(self, pool: LevelPool) -> None:
         """Evaluate the problem's initial condition once per band of patches
@@ -703,7 +718,10 @@ class Simulation:
             self._sync_status(f"at t={self.time:.6g}")
         with self._timed("mass+finite"):
             mass = self.composite_mass()
-        event = (self.delta_acc[:2].sum(dim=0) - before).cpu().numpy()
+        with torch.cuda.stream(self.stream):
+            ev = self.delta_acc[:2].sum(dim=0) - before
+            self._reduce_event(ev)
+        event = ev.cpu().numpy()
         self.d2h_bytes += 8 * self.M
         sync = mass - self._mass_prev - event
         if not self.stats.sync_delta:
@@ -713,6 +731,10 @@ class Simulation:
         self._mass_prev = mass
         self.stats.num_coarse_steps += 1
         self._sync_status(f"at t={self.time:.6g}")
+
+    def _reduce_event(self, ev: torch.Tensor) -> None:
+        """Single GPU: the refine/derefine delta of this coarse step is
+        already global (the sharded driver all-reduces it, since mass is)."""
 
     def run(self, n_coarse: int) -> RunStats:
         for _ in range(n_coarse):
@@ -755,19 +777,22 @@ class Simulation:
         return self.finish()
 
     def finish(self) -> RunStats:
+        """RunStats with the device accumulators folded in (idempotent: the
+        fields are recomputed from the accumulators on every call)."""
         self.stream.synchronize()
-        acc = self.acc.cpu().numpy()
+        return self._fill_stats(self.stats, self.acc.cpu().numpy(), self.delta_acc.cpu().numpy())
+
+    def _fill_stats(self, st: RunStats, acc: np.ndarray, d: np.ndarray) -> RunStats:
         M = self.M
-        self.stats.clipped_mass = list(acc[:M])
-        self.stats.hyperbolicity_warnings = int(round(acc[M]))
-        self.stats.wet_prefix_repairs = int(round(acc[M + 1]))
-        d = self.delta_acc.cpu().numpy()
-        self.stats.refine_delta = list(d[0])
-        self.stats.derefine_delta = list(d[1])
-        self.stats.final_mass = list(self._mass_prev)
-        if self.stats.initial_mass:
-            self.stats.mass_drift = [f - i for f, i in zip(self.stats.final_mass, self.stats.initial_mass)]
-        return self.stats
+        st.clipped_mass = list(acc[:M])
+        st.hyperbolicity_warnings = int(round(acc[M]))
+        st.wet_prefix_repairs = int(round(acc[M + 1]))
+        st.refine_delta = list(d[0])
+        st.derefine_delta = list(d[1])
+        st.final_mass = list(self._mass_prev)
+        if st.initial_mass:
+            st.mass_drift = [f - i for f, i in zip(st.final_mass, st.initial_mass)]
+        return st
 
     # -- checkpoint: host snapshot / restore (pinned host buffers) ----------------------------
     def _interior_base(self, pool: LevelPool):
@@ -787,7 +812,7 @@ class Simulation:
         ``bathymetry=True``; a restore re-derives it otherwise."""
         snap = {"time": self.time, "steps": dict(self.steps), "specs": list(self.specs), "levels": {},
                 "acc": None, "delta_acc": None, "mass_prev": np.array(self._mass_prev),
-                "stats": replace(self.stats)}
+                "stats": copy.deepcopy(self.stats)}
         nbytes = 0
         with torch.cuda.stream(self.stream):
             from .device import pinned_acquire
@@ -857,7 +882,7 @@ class Simulation:
         self.time = snap["time"]
         self.steps = dict(snap["steps"])
         self.specs = list(snap["specs"])
-        self.stats = replace(snap["stats"])
+        self.stats = copy.deepcopy(snap["stats"])
         nbytes = 0
         for lev in sorted(snap["levels"]):
             d = snap["levels"][lev]

@@ -31,8 +31,7 @@ MAGIC_TEXT = "MLAMR FRAME-TEXT"
 _REC_HDR = struct.Struct("<5q")
 
 
-class FrameFormatError(ValueError):
-    """Malformed or incompatible frame (errors.FrameFormatError of the reference)."""
+from .errors import FrameFormatError  # noqa: E402,F401  (the reference's class when importable)
 
 
 # -- writing ------------------------------------------------------------------------------

@@ -11,6 +11,7 @@ one, mutating the arrays in place exactly like the reference:
 * :func:`interpolate_state` refine.interpolate_state  (refine.py:158-190)
 * :func:`refine_patch`      refine.refine_patch       (refine.py:193-239)
 * :func:`average_down`      coarsen.average_down      (coarsen.py:30-76)
+* :func:`check_bathymetry_consistency`  coarsen.check_bathymetry_consistency (coarsen.py:79-100)
 * :func:`fill_ghosts`       ghost.fill_ghosts         (ghost.py:156-197)
 
 They exist for integration and per-operation parity; the level-batched
@@ -302,6 +303,28 @@ def average_down(fine_patches, coarse_patches, r_x: int, r_y: int, params, check
     for p, b0 in zip(coarse_patches, before):
         delta += (p.h[:, g:-g, g:-g] - b0).sum(axis=(1, 2)) * (dxc * dyc)
     return delta
+
+
+def check_bathymetry_consistency(fine_patch, coarse_patches, r_x: int, r_y: int, atol: float = 1e-12) -> None:
+    """coarsen.check_bathymetry_consistency (coarsen.py:79-100) on the GPU
+    (mlamr_check_bathymetry): AssertionError when a covered coarse
+    bathymetry value is not the block mean of its fine values."""
+    if not coarse_patches:
+        return
+    fb = _box(fine_patch)
+    cb = [_box(p) for p in coarse_patches]
+    dxc, dyc = _dxdy(coarse_patches[0])
+    dxf, dyf = _dxdy(fine_patch)
+    coarse = _pool_for(coarse_patches, max(b.hi_i for b in cb) + 1, max(b.hi_j for b in cb) + 1, dxc, dyc, 1)
+    fine = _pool_for([fine_patch], fb.hi_i + 1, fb.hi_j + 1, dxf, dyf, 1)
+    status = torch.zeros(1, dtype=torch.int32, device="cuda")
+    bad = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device="cuda")
+    cbase, n = fine.coarse_base(r_x, r_y)
+    N.check(N.lib().mlamr_check_bathymetry(fine.struct(), coarse.struct(), r_x, r_y, float(atol), cbase.data_ptr(),
+                                           n, status.data_ptr(), bad.data_ptr(),
+                                           torch.cuda.current_stream().cuda_stream), "check_bathymetry")
+    if int(status.item()) & N.ST_BATHY:
+        raise AssertionError(f"bathymetry ladder does not telescope under {tuple(fb)}")
 
 
 def fill_ghosts(patch, siblings, parent_provider, boundaries, level_box, r_x: int, r_y: int, params) -> None:

@@ -24,6 +24,7 @@ Differences from the single-GPU driver, all confined to this subclass:
 
 from __future__ import annotations
 
+import copy
 from math import prod
 
 import numpy as np
@@ -307,14 +308,32 @@ class ShardedSimulation(Simulation):
         return np.array([0.0 if b < 0 else np.array([b], np.int64).view(np.float64)[0]])
 
     def finish(self):
+        """Global RunStats of the job: the accumulators, total and per-level
+        cell counts are all-reduced into temporaries and returned in a copy,
+        so this rank's live accumulators and ``self.stats`` keep counting
+        their own patches (finish() may be called any number of times)."""
+        levels = [s.level for s in self.specs]
         with torch.cuda.stream(self.stream):
-            self.comm.allreduce(self.acc)
-            self.comm.allreduce(self.delta_acc)
-            cells = torch.tensor([float(self.stats.total_cell_updates)], dtype=torch.float64, device=self.dev)
+            acc = self.acc.clone()
+            dacc = self.delta_acc.clone()
+            self.comm.allreduce(acc)
+            self.comm.allreduce(dacc)
+            cells = torch.tensor([float(self.stats.total_cell_updates)]
+                                 + [float(self.stats.cell_updates_per_level.get(l, 0)) for l in levels],
+                                 dtype=torch.float64, device=self.dev)
             self.comm.allreduce(cells)
-        st = super().finish()
-        st.total_cell_updates = int(cells.item())
+        self.stream.synchronize()
+        st = self._fill_stats(copy.deepcopy(self.stats), acc.cpu().numpy(), dacc.cpu().numpy())
+        c = [int(v) for v in cells.cpu().tolist()]
+        st.total_cell_updates = c[0]
+        st.cell_updates_per_level = {l: n for l, n in zip(levels, c[1:]) if n}
         return st
+
+    def _reduce_event(self, ev: torch.Tensor) -> None:
+        """The refine/derefine deltas accumulate over owned patches only,
+        while the composite mass is global: the per-step event delta must be
+        global too before sync = mass - mass_prev - event (driver.py:303-307)."""
+        self.comm.allreduce(ev)
 
     # -- flags over owned patches, all-reduced -----------------------------------------
     def _reduce_flag_bits(self, bits) -> None:

@@ -91,7 +91,20 @@ def main():
         assert fb is None
     a, b = ref.finish(), sh.finish()
     assert a.total_cell_updates == b.total_cell_updates, (a.total_cell_updates, b.total_cell_updates)
+    assert a.cell_updates_per_level == b.cell_updates_per_level, (a.cell_updates_per_level,
+                                                                  b.cell_updates_per_level)
     assert a.num_regrids == b.num_regrids
+    # sync_delta = mass - mass_prev - (refine + derefine delta) per coarse step
+    # (driver.py:303-307): the sharded event delta is all-reduced like the mass
+    scale = float(np.abs(ref.composite_mass()).sum())
+    np.testing.assert_allclose(b.sync_delta, a.sync_delta, rtol=0, atol=1e-11 * scale)
+    for x, y in ((a.refine_delta, b.refine_delta), (a.derefine_delta, b.derefine_delta),
+                 (a.clipped_mass, b.clipped_mass)):
+        np.testing.assert_allclose(np.asarray(y, float), np.asarray(x, float), rtol=0, atol=1e-11 * scale)
+    # finish() is idempotent: a second call returns the same global numbers
+    c = sh.finish()
+    assert c.total_cell_updates == b.total_cell_updates and c.cell_updates_per_level == b.cell_updates_per_level
+    assert c.refine_delta == b.refine_delta and c.clipped_mass == b.clipped_mass
     np.testing.assert_allclose(sh.composite_mass(), ref.composite_mass(), rtol=1e-12)
     print(f"rank {rank}: {name} sharded == single-GPU ({steps} steps, exchanged {sh.bytes_exchanged} B, "
           f"owned {[int(p.n_owned) for p in sh.levels.values()]} of {[len(v) for v in sh.layout.values()]})",

@@ -142,6 +142,11 @@ def test_snapshot_restore_continues_bit_identically(bathymetry):
         a.advance_coarse_step(dt)
         b.advance_coarse_step(dt)
     assert a.time == b.time and a.stats.total_cell_updates == b.stats.total_cell_updates
+    # the snapshot is a deep copy: the two runs' counters are their own
+    assert a.stats.cell_updates_per_level == b.stats.cell_updates_per_level
+    assert a.stats.sync_delta == b.stats.sync_delta
+    assert a.stats.cell_updates_per_level is not b.stats.cell_updates_per_level
+    assert snap["stats"].cell_updates_per_level != a.stats.cell_updates_per_level
     for lev in range(1, a.L + 1):
         fa, fb = a.patch_fields(lev), b.patch_fields(lev)
         assert [x[0] for x in fa] == [x[0] for x in fb]
