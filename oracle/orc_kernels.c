@@ -482,20 +482,53 @@ int orc_interpolate_state(int M, const double *ch, const double *chu, const doub
     return ORC_OK;
 }
 
+/* numpy's pairwise_sum over n contiguous doubles (numpy/_core/src/umath/
+ * loops_utils.h.src): sequential from 0.0 below 8 elements, else eight
+ * running accumulators combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus
+ * a sequential tail (n <= 128 here). */
+static double np_pairwise(const double *a, int n)
+{
+    if (n < 8) {
+        double res = 0.0;
+        for (int i = 0; i < n; ++i) res = res + a[i];
+        return res;
+    }
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] = r[j] + a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res = res + a[i];
+    return res;
+}
+
 /* coarsen.block_mean (coarsen.py:21-27) in numpy's evaluation order for
- * r <= 4: per fine row a sequential sum over p, rows summed sequentially
- * over q, then one divide by r_x*r_y.  src has row stride src_stride. */
+ * r <= 4 (SURVEY probe 2, extended): the reduction over axes (-3, -1) of
+ * the (.., cny, r_y, cnx, r_x) view sums, per fine row, sequentially over p,
+ * then the row sums sequentially over q -- unless the patch is ONE coarse
+ * cell wide (cnx == 1): numpy then coalesces the r_y x r_x block into one
+ * contiguous run of r_x*r_y elements and sums it with pairwise_sum.  One
+ * divide by r_x*r_y either way.  src has row stride src_stride. */
 void orc_block_mean(const double *src, long src_stride, int cnx, int cny,
                     int r_x, int r_y, double *dst, long dst_stride)
 {
+    double blk[64];
     for (int J = 0; J < cny; ++J)
         for (int I = 0; I < cnx; ++I) {
             double s = 0.0;
-            for (int q = 0; q < r_y; ++q) {
-                const double *row = src + (long)(J * r_y + q) * src_stride + (long)I * r_x;
-                double rs = row[0];
-                for (int pp = 1; pp < r_x; ++pp) rs = rs + row[pp];
-                s = (q == 0) ? rs : s + rs;
+            if (cnx == 1 && r_x * r_y <= 64) {
+                for (int q = 0; q < r_y; ++q)
+                    for (int pp = 0; pp < r_x; ++pp)
+                        blk[q * r_x + pp] = src[(long)(J * r_y + q) * src_stride + (long)I * r_x + pp];
+                s = np_pairwise(blk, r_x * r_y);
+            } else {
+                for (int q = 0; q < r_y; ++q) {
+                    const double *row = src + (long)(J * r_y + q) * src_stride + (long)I * r_x;
+                    double rs = row[0];
+                    for (int pp = 1; pp < r_x; ++pp) rs = rs + row[pp];
+                    s = (q == 0) ? rs : s + rs;
+                }
             }
             dst[(long)J * dst_stride + I] = s / (double)(r_x * r_y);
         }

@@ -421,6 +421,30 @@ __global__ void __launch_bounds__(NTA) k_fill_bathy(mlamr_level lv, const double
 // One coarse cell of average_down: block-mean the fine children of coarse
 // cell (clo_i + I, clo_j + J) into the coarse owner's interior (if any) and
 // accumulate the mass change into dsum.
+// numpy's pairwise_sum over n contiguous doubles (numpy/_core/src/umath/
+// loops_utils.h.src), n <= 128: sequential from 0.0 below 8 elements, else
+// eight running accumulators, ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then a
+// sequential tail.  block_mean of a patch ONE coarse cell wide sums its
+// r_y x r_x block this way (numpy coalesces the two reduced axes into one
+// contiguous run); wider patches use the per-row-then-rows order.
+__device__ __forceinline__ double np_pairwise(const double *a, int n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int i = 0; i < n; ++i) res = res + a[i];
+        return res;
+    }
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = r[j] + a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res = res + a[i];
+    return res;
+}
+
 template <int M, int RX, int RY>
 __device__ __forceinline__ void avg_cell(const mlamr_level &fine, const mlamr_level &coarse, const PatchView &fv,
                                          int r_x, int r_y, int cnx, int clo_i, int clo_j, int idx, double tol,
@@ -459,13 +483,22 @@ __device__ __forceinline__ void avg_cell(const mlamr_level &fine, const mlamr_le
 #pragma unroll
                             for (int pp = 0; pp < (RX > 0 ? RX : 1); ++pp) v[q][pp] = a[(int64_t)q * fv.NX + pp];
                     }
+                    if (cnx == 1) {
+                        s = np_pairwise(&v[0][0], (RY > 0 ? RY : 1) * (RX > 0 ? RX : 1));
+                    } else {
 #pragma unroll
-                    for (int q = 0; q < (RY > 0 ? RY : 1); ++q) {
-                        double rs = v[q][0];
+                        for (int q = 0; q < (RY > 0 ? RY : 1); ++q) {
+                            double rs = v[q][0];
 #pragma unroll
-                        for (int pp = 1; pp < (RX > 0 ? RX : 1); ++pp) rs = rs + v[q][pp];
-                        s = (q == 0) ? rs : s + rs;
+                            for (int pp = 1; pp < (RX > 0 ? RX : 1); ++pp) rs = rs + v[q][pp];
+                            s = (q == 0) ? rs : s + rs;
+                        }
                     }
+                } else if (cnx == 1 && r_x * r_y <= 64) {
+                    double blk[64];
+                    for (int q = 0; q < r_y; ++q)
+                        for (int pp = 0; pp < r_x; ++pp) blk[q * r_x + pp] = a[(int64_t)q * fv.NX + pp];
+                    s = np_pairwise(blk, r_x * r_y);
                 } else {
                     for (int q = 0; q < r_y; ++q) {
                         const double *row = a + (int64_t)q * fv.NX;
@@ -587,10 +620,17 @@ __global__ void __launch_bounds__(NTA) k_check_bathy(mlamr_level fine, mlamr_lev
         if (o < 0) continue;
         const double *a = fine.bathy + fv.off + (int64_t)(MLAMR_G + J * r_y) * fv.NX + (MLAMR_G + I * r_x);
         double s = 0.0;
-        for (int q = 0; q < r_y; ++q) {
-            double rs = a[(int64_t)q * fv.NX];
-            for (int pp = 1; pp < r_x; ++pp) rs = rs + a[(int64_t)q * fv.NX + pp];
-            s = (q == 0) ? rs : s + rs;
+        if (cnx == 1 && r_x * r_y <= 64) {   // numpy's coalesced block (np_pairwise)
+            double blk[64];
+            for (int q = 0; q < r_y; ++q)
+                for (int pp = 0; pp < r_x; ++pp) blk[q * r_x + pp] = a[(int64_t)q * fv.NX + pp];
+            s = np_pairwise(blk, r_x * r_y);
+        } else {
+            for (int q = 0; q < r_y; ++q) {
+                double rs = a[(int64_t)q * fv.NX];
+                for (int pp = 1; pp < r_x; ++pp) rs = rs + a[(int64_t)q * fv.NX + pp];
+                s = (q == 0) ? rs : s + rs;
+            }
         }
         const double mean = s / nblk;
         const int32_t *b = coarse.box + 4 * o;

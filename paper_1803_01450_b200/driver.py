@@ -260,6 +260,9 @@ class Simulation:
 
     def _sync_status(self, where: str = "") -> None:
         self.d2h_bytes += 4
+        # the status word is written on the driver stream, which need not
+        # be the caller's current stream (torch streams are non-blocking)
+        self.stream.synchronize()
         st = int(self.status.item())
         if st:
             bad = int(self.bad.item())
@@ -721,7 +724,7 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             ev = self.delta_acc[:2].sum(dim=0) - before
             self._reduce_event(ev)
-        event = ev.cpu().numpy()
+            event = ev.cpu().numpy()   # ordered after ev on the driver stream
         self.d2h_bytes += 8 * self.M
         sync = mass - self._mass_prev - event
         if not self.stats.sync_delta:

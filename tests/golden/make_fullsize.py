@@ -51,6 +51,31 @@ def problem(name: str):
     return problems.CONFIGS[name]()
 
 
+def ref_variant(name: str):
+    """(problem, coarse steps) of the configurations the REFERENCE itself
+    runs (make_refruns.py): C1 and C2 at full size (C2 over its whole
+    50-step schedule), C4 and C5 reduced to L1 64x64 (the reference's O(P^2)
+    scans), with the regrid settings of the GPU parity variants
+    (tests/test_gpu_driver.py)."""
+    from paper_1803_01450_b200 import problems
+    if name == "C1":
+        return problems.config1(), 3
+    if name == "C2":
+        return problems.config2(), 50
+    if name == "C4r":
+        pb = problems.config4(nx0=64)
+        pb.regrid_interval = 2
+        return pb, 3
+    if name == "C5r":
+        pb = problems.config5(nx0=64)
+        pb.bernoulli = (0.05,)
+        pb.flag_rule = ("bernoulli", 0.05, 1)
+        # the reference's CFL guard aborts coarse step 4 (Courant 1.193 on a
+        # freshly refined level-2 patch): the fixture pins that abort too
+        return pb, 4
+    raise KeyError(name)
+
+
 DIGEST_BYTES = 8
 
 

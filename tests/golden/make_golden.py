@@ -188,6 +188,19 @@ def make_blockmean_cases(rng):
         recs[f"c{k}_r"] = np.array([rx, ry])
         recs[f"c{k}_out"] = coarsen.block_mean(a, rx, ry)
         k += 1
+    # patches ONE coarse cell wide (numpy then sums each r_y x r_x block as
+    # one contiguous pairwise run) and one coarse cell tall, in a strided
+    # view like average_down's fp.h[:, fjj, fii] (coarsen.py:59); own rng so
+    # the fixtures generated after this one keep their inputs
+    nr = np.random.default_rng(1803)
+    for (rx, ry) in ((2, 2), (4, 4), (4, 2), (2, 4), (4, 1), (2, 1)):
+        for (cny, cnx) in ((5, 1), (1, 1), (1, 6), (3, 2)):
+            big = nr.standard_normal((2, ry * cny + 4, rx * cnx + 4)) * nr.uniform(0, 1e3, (2, ry * cny + 4, rx * cnx + 4))
+            a = big[:, 2:-2, 2:-2]
+            recs[f"c{k}_a"] = np.ascontiguousarray(a)
+            recs[f"c{k}_r"] = np.array([rx, ry])
+            recs[f"c{k}_out"] = coarsen.block_mean(a, rx, ry)
+            k += 1
     recs["ncases"] = np.asarray(k)
     _save("blockmean_cases.npz", **recs)
 

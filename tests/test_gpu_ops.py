@@ -136,3 +136,28 @@ def test_average_down_and_refine_shims_match_oracle(oracle):
     d_g = ops.refine_patch(c_g, p_g, 2, 2, prm)
     assert same(p_o.h, p_g.h) and same(p_o.hu, p_g.hu) and same(p_o.hv, p_g.hv)
     np.testing.assert_allclose(d_g, d_o, rtol=1e-12, atol=1e-12)
+
+
+def test_average_down_block_means_match_reference_bitwise():
+    """coarsen.block_mean (coarsen.py:21-27) as average_down evaluates it on
+    the GPU, against the reference's own outputs: every ratio, including
+    patches one coarse cell wide, whose r_y x r_x blocks numpy sums as one
+    contiguous pairwise run (tests/golden/make_golden.py)."""
+    from paper_1803_01450_b200 import ops
+    z = load_golden("blockmean_cases.npz")
+    for k in range(int(z["ncases"])):
+        a = z[f"c{k}_a"]
+        rx, ry = (int(v) for v in z[f"c{k}_r"])
+        M, ny, nx = a.shape
+        cny, cnx = ny // ry, nx // rx
+        pad = lambda x: np.pad(x, ((0, 0), (2, 2), (2, 2)))  # noqa: E731
+        fine = HostPatch((rx * 3, ry * 2, rx * 3 + nx - 1, ry * 2 + ny - 1), 1.0 / rx, 1.0 / ry,
+                         pad(np.abs(a)), pad(a), pad(-a), np.zeros((ny + 4, nx + 4)))
+        coarse = HostPatch((0, 0, cnx + 5, cny + 5), 1.0, 1.0, np.zeros((M, cny + 10, cnx + 10)),
+                           np.zeros((M, cny + 10, cnx + 10)), np.zeros((M, cny + 10, cnx + 10)),
+                           np.zeros((cny + 10, cnx + 10)))
+        ops.average_down([fine], [coarse], rx, ry, _Params(M, (0.95, 1.0)), check_time=False)
+        got = coarse.hu[:, 2 + 2:2 + 2 + cny, 2 + 3:2 + 3 + cnx]
+        want = z[f"c{k}_out"]
+        dry = coarse.h[:, 2 + 2:2 + 2 + cny, 2 + 3:2 + 3 + cnx] <= 1e-3
+        assert same(got[~dry], want[~dry]), (k, rx, ry, a.shape, mismatch(got[~dry], want[~dry]))
