@@ -141,6 +141,12 @@ int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                const int32_t *status, const int64_t *ghost_base, const int64_t *ghost_plan,
                void *stream);
 
+/* Select the K1 form for 32-column tiles and M <= 2: 0 = phase kernel
+ * (default; per-cell phases between block barriers), 1 = line walker
+ * (bit-identical, one interface per register window; env MLAMR_STEP=walk).
+ * Returns the previous form, or -1 for an unknown one. */
+int mlamr_set_step_form(int form);
+
 /* Interior tile shape (rows, columns) the step kernel uses for a level
  * whose widest patch interior is max_patch_nx cells and num_layers layers;
  * the host builds that level's `tiles` with it and passes tx as tile_tx. */

@@ -105,6 +105,7 @@ SIGNATURES = {
     "mlamr_chop_boxes": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                         c_vp, ctypes.c_int]),
     "mlamr_step_tile": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_vp, c_vp]),
+    "mlamr_set_step_form": (ctypes.c_int, [ctypes.c_int]),
     "mlamr_boxes_meet_any": (ctypes.c_int, [c_vp, ctypes.c_int, c_vp, ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_selftest_div": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, c_vp, c_vp, c_vp]),
     "mlamr_flags_bernoulli": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong,

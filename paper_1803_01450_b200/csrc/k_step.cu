@@ -17,7 +17,10 @@
 // compiled with -fmad=false, so results are bit-identical to the numba
 // reference (which does not contract either).
 
+#include <atomic>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <map>
 #include <mutex>
 
@@ -72,6 +75,20 @@ struct StepConst {
 #undef MLAMR_STEP_TY
 #undef MLAMR_STEP_NT
 #undef MLAMR_STEP_MINB
+
+// K1 line-walker form for the wide tiles (M <= 2): step_walk.cuh
+#include "step_walk.cuh"
+
+// Which K1 form runs the wide tiles.  The phase form is the default: the
+// walker is bit-identical but measured slower on C4 (3.74 vs 3.07 ms per
+// level-3 launch; profiles/r02/README.md).  MLAMR_STEP=walk or
+// mlamr_set_step_form(1) selects the walker.
+static int step_form_init() {
+    const char *e = getenv("MLAMR_STEP");
+    return (e && strcmp(e, "walk") == 0) ? 1 : 0;
+}
+static std::atomic<int> g_step_form{step_form_init()};
+static bool use_walker() { return g_step_form.load(std::memory_order_relaxed) == 1; }
 
 // CFL guard + deterministic reduction of the step partials.  FIN_BLOCKS
 // CTAs each reduce a fixed contiguous chunk of tiles into chunk[b][q]; the
@@ -184,10 +201,20 @@ static int launch_step_shape(int tile_tx, const mlamr_level &lv, const double *s
     if (tile_tx == narrow::TX)
         return narrow::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
                                       gbase, gplan, st);
+    if constexpr (M <= 2) {
+        if (tile_tx == wide::TX && use_walker())
+            return walk::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc,
+                                        status, gbase, gplan, st);
+    }
     if (tile_tx == wide::TX)
         return wide::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
                                     gbase, gplan, st);
     return -3;
+}
+
+extern "C" int mlamr_set_step_form(int form) {
+    if (form != 0 && form != 1) return -1;
+    return g_step_form.exchange(form);
 }
 
 extern "C" int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,

@@ -155,3 +155,26 @@ def test_snapshot_restore_continues_bit_identically(bathymetry):
                 assert np.array_equal(u[:, 2:-2, 2:-2], v[:, 2:-2, 2:-2])
             assert np.array_equal(x[4], y[4])
     np.testing.assert_array_equal(a.composite_mass(), b.composite_mass())
+
+
+@pytest.mark.parametrize("name", ["C2", "C4"])
+def test_walker_step_form_matches_oracle(oracle, name):
+    """The line-walker form of K1 (csrc/step_walk.cuh, mlamr_set_step_form)
+    is bit-identical to the oracle on the wide-tile configs."""
+    from paper_1803_01450_b200 import _native as N
+    from paper_1803_01450_b200.driver import Simulation
+    prev = N.lib().mlamr_set_step_form(1)
+    try:
+        pb, steps = _variant(name)
+        gpu = Simulation(pb)
+        cpu = oracle.Simulation(pb)
+        for _ in range(steps):
+            dt = cpu.choose_dt()
+            assert gpu.choose_dt() == dt
+            cpu.apply_dynamic_rt(dt)
+            gpu.apply_dynamic_rt(dt)
+            cpu.advance_coarse_step(dt)
+            gpu.advance_coarse_step(dt)
+            assert compare_levels(gpu, cpu) == []
+    finally:
+        N.lib().mlamr_set_step_form(prev)
