@@ -159,9 +159,17 @@ int mlamr_step_tile(int max_patch_nx, int num_layers, int *ty, int *tx);
  * min-ed into *bad_patch. */
 int mlamr_step_finalize(mlamr_level lv, const double *src_state, double *dst_state,
                         const int32_t *tiles, int n_tiles, double dt,
-                        mlamr_params prm, const long long *speed_bits,
+                        mlamr_params prm, long long *speed_bits,
                         const double *tile_acc, double *acc, int32_t *status,
-                        int32_t *bad_patch, void *stream);
+                        int32_t *bad_patch, int reset_speeds, void *stream);
+
+/* Deterministic column sums of per-block partials (row-major [rows][cols]):
+ * s_c = (sum over rows, fixed order) * scale; acc[c] = init ? s_c : acc[c]
+ * + s_c, and acc2[c] += s_c when acc2 is given.  One launch in place of the
+ * framework reductions the driver used for mass and refine/derefine
+ * deltas. */
+int mlamr_sum_partials(const double *part, long long rows, int cols, double scale, double *acc,
+                       double *acc2, int init, void *stream);
 
 /* ---- K6: per-patch observed max wave speed (physics.py:261-278) --------- */
 int mlamr_max_speed_tiles(mlamr_level lv, const double *state, const int32_t *tiles,
@@ -186,13 +194,21 @@ int mlamr_fill_ghosts(mlamr_level lv, const mlamr_level *parent,
  * (outside the level box, boundary condition).  mlamr_fill_ghosts_planned
  * then copies sibling cells, interpolates the compacted `interp_cells`
  * (int32 pairs patch, ghost index) from the (blended) parent and applies
- * the BCs of `bc_patches` -- the same values as mlamr_fill_ghosts. */
+ * the BCs of `bc_patches` -- the same values as mlamr_fill_ghosts.  With
+ * `n_interp_dev` (device int32, e.g. from mlamr_plan_interp_cells) the
+ * list's length is read on the device and n_interp is its capacity; NULL =
+ * n_interp cells.  mlamr_plan_interp_cells compacts the plan's -1 cells of
+ * the listed patches (NULL = all) into `cells` (int32 pairs, unordered) and
+ * their number into *count, without a host round trip. */
 int mlamr_ghost_plan(mlamr_level lv, const int64_t *gbase, int64_t *plan, int max_ghost, void *stream);
+int mlamr_plan_interp_cells(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
+                            const int32_t *patch_list, int n_list, int max_ghost, int32_t *cells,
+                            int32_t *count, void *stream);
 int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *parent, const double *parent_old_state,
                               double theta, int r_x, int r_y, const int32_t *bcs, mlamr_params prm,
                               const int32_t *status, const int64_t *gbase, const int64_t *plan,
                               const int32_t *patch_list, int n_list, int max_ghost,
-                              const int32_t *interp_cells, int n_interp,
+                              const int32_t *interp_cells, int n_interp, const int32_t *n_interp_dev,
                               const int32_t *bc_patches, int n_bc, void *stream);
 
 /* Patch bathymetry (frame included) from a level-wide array of in-domain

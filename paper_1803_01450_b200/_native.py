@@ -66,7 +66,9 @@ SIGNATURES = {
     "mlamr_step": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double,
                                   ctypes.c_int, Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_step_finalize": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_double,
-                                           Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+                                           Params, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
+    "mlamr_sum_partials": (ctypes.c_int, [c_vp, ctypes.c_longlong, ctypes.c_int, ctypes.c_double, c_vp, c_vp,
+                                          ctypes.c_int, c_vp]),
     "mlamr_max_speed_tiles": (ctypes.c_int, [Level, c_vp, c_vp, ctypes.c_int, ctypes.c_int, Params, c_vp, c_vp]),
     "mlamr_fill_ghosts": (ctypes.c_int, [Level, ctypes.POINTER(Level), c_vp, ctypes.c_double,
                                          ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp,
@@ -75,7 +77,9 @@ SIGNATURES = {
     "mlamr_fill_ghosts_planned": (ctypes.c_int, [Level, ctypes.POINTER(Level), c_vp, ctypes.c_double,
                                                  ctypes.c_int, ctypes.c_int, c_i32p, Params, c_vp, c_vp, c_vp,
                                                  c_vp, ctypes.c_int, ctypes.c_int, c_vp, ctypes.c_int, c_vp,
-                                                 ctypes.c_int, c_vp]),
+                                                 c_vp, ctypes.c_int, c_vp]),
+    "mlamr_plan_interp_cells": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_int, c_vp, c_vp,
+                                               c_vp]),
     "mlamr_fill_bathymetry": (ctypes.c_int, [Level, c_vp, c_i32p, c_vp]),
     "mlamr_average_down": (ctypes.c_int, [Level, Level, ctypes.c_int, ctypes.c_int, Params, c_vp,
                                           ctypes.c_int, c_vp, c_vp]),

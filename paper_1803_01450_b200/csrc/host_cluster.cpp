@@ -121,53 +121,107 @@ struct Prefix {
 
 }  // namespace
 
-static int cluster_recursion(const Prefix &F, const Prefix *BADp, int ny, int nx, double eff,
-                             int32_t *out_boxes, int max_boxes) {
-    const bool have_allowed = BADp != nullptr;
-    struct Node { int i0, j0, i1, j1; };
-    std::vector<Node> stack;
-    std::vector<std::array<int, 4>> boxes;
-    if (ny > 0 && nx > 0) stack.push_back({0, 0, nx - 1, ny - 1});
+// One node of the bisection: trim to the flags' bounding box, accept it
+// (efficiency, or a single cell, or no valid cut) or split it in two.
+// Returns 0 (dropped: no flags), 1 (accepted into `out`), 2 (split into
+// l and r).
+struct Node { int i0, j0, i1, j1; };
+
+static int cluster_node(const Prefix &F, const Prefix *BADp, double eff, const Node &nd, std::array<int, 4> &out,
+                        Node &l, Node &r, std::vector<int64_t> &sx, std::vector<int64_t> &sy) {
+    if (F.box(nd.i0, nd.j0, nd.i1, nd.j1) == 0) return 0;
+    int a_j = nd.j0, b_j = nd.j1, a_i = nd.i0, b_i = nd.i1;
+    while (F.rowsum(a_j, nd.i0, nd.i1) == 0) ++a_j;
+    while (F.rowsum(b_j, nd.i0, nd.i1) == 0) --b_j;
+    while (F.colsum(a_i, nd.j0, nd.j1) == 0) ++a_i;
+    while (F.colsum(b_i, nd.j0, nd.j1) == 0) --b_i;
+    const int64_t nflag = F.box(a_i, a_j, b_i, b_j);
+    const int w = b_i - a_i + 1, h = b_j - a_j + 1;
+    const int64_t area = (int64_t)w * h;
+    const bool ok = BADp == nullptr || BADp->box(a_i, a_j, b_i, b_j) == 0;
+    out = {a_i, a_j, b_i, b_j};
+    if (area == 1 || (ok && (double)nflag >= eff * (double)area)) return 1;
+    sx.resize(w);
+    sy.resize(h);
+    for (int i = 0; i < w; ++i) sx[i] = F.colsum(a_i + i, a_j, b_j);
+    for (int j = 0; j < h; ++j) sy[j] = F.rowsum(a_j + j, a_i, b_i);
+    const Cut cx = signature_cut(sx);
+    const Cut cy = signature_cut(sy);
+    if (!cx.valid && !cy.valid) return 1;
+    const int qx = cx.valid ? cx.quality : -1, nxs = cx.valid ? w : 0;
+    const int qy = cy.valid ? cy.quality : -1, nys = cy.valid ? h : 0;
+    const bool cut_x = (qx > qy) || (qx == qy && nxs >= nys);
+    if (cut_x) {
+        l = {a_i, a_j, a_i + cx.index - 1, b_j};
+        r = {a_i + cx.index, a_j, b_i, b_j};
+    } else {
+        l = {a_i, a_j, b_i, a_j + cy.index - 1};
+        r = {a_i, a_j + cy.index, b_i, b_j};
+    }
+    return 2;
+}
+
+// Sub-trees below this many cells are bisected by the task that reached them.
+constexpr int64_t kTaskCells = 1 << 14;
+
+static void cluster_subtree(const Prefix &F, const Prefix *BADp, double eff, Node root,
+                            std::vector<std::array<int, 4>> &boxes) {
+    std::vector<Node> stack{root};
     std::vector<int64_t> sx, sy;
     while (!stack.empty()) {
-        Node nd = stack.back();
+        const Node nd = stack.back();
         stack.pop_back();
-        if (F.box(nd.i0, nd.j0, nd.i1, nd.j1) == 0) continue;
-        int a_j = nd.j0, b_j = nd.j1, a_i = nd.i0, b_i = nd.i1;
-        while (F.rowsum(a_j, nd.i0, nd.i1) == 0) ++a_j;
-        while (F.rowsum(b_j, nd.i0, nd.i1) == 0) --b_j;
-        while (F.colsum(a_i, nd.j0, nd.j1) == 0) ++a_i;
-        while (F.colsum(b_i, nd.j0, nd.j1) == 0) --b_i;
-        const int64_t nflag = F.box(a_i, a_j, b_i, b_j);
-        const int w = b_i - a_i + 1, h = b_j - a_j + 1;
-        const int64_t area = (int64_t)w * h;
-        const bool ok = !have_allowed || BADp->box(a_i, a_j, b_i, b_j) == 0;
-        if (area == 1 || (ok && (double)nflag >= eff * (double)area)) {
-            boxes.push_back({a_i, a_j, b_i, b_j});
-            continue;
-        }
-        sx.resize(w);
-        sy.resize(h);
-        for (int i = 0; i < w; ++i) sx[i] = F.colsum(a_i + i, a_j, b_j);
-        for (int j = 0; j < h; ++j) sy[j] = F.rowsum(a_j + j, a_i, b_i);
-        const Cut cx = signature_cut(sx);
-        const Cut cy = signature_cut(sy);
-        if (!cx.valid && !cy.valid) {
-            boxes.push_back({a_i, a_j, b_i, b_j});
-            continue;
-        }
-        const int qx = cx.valid ? cx.quality : -1, nxs = cx.valid ? w : 0;
-        const int qy = cy.valid ? cy.quality : -1, nys = cy.valid ? h : 0;
-        const bool cut_x = (qx > qy) || (qx == qy && nxs >= nys);
-        if (cut_x) {
-            stack.push_back({a_i + cx.index, a_j, b_i, b_j});
-            stack.push_back({a_i, a_j, a_i + cx.index - 1, b_j});
-        } else {
-            stack.push_back({a_i, a_j + cy.index, b_i, b_j});
-            stack.push_back({a_i, a_j, b_i, a_j + cy.index - 1});
+        std::array<int, 4> bx;
+        Node l, r;
+        const int k = cluster_node(F, BADp, eff, nd, bx, l, r, sx, sy);
+        if (k == 1) boxes.push_back(bx);
+        if (k == 2) {
+            stack.push_back(r);
+            stack.push_back(l);
         }
     }
-    std::stable_sort(boxes.begin(), boxes.end(), [](const std::array<int, 4> &a, const std::array<int, 4> &b) {
+}
+
+// The bisection tree is walked by OpenMP tasks down to kTaskCells-sized
+// nodes, each finishing its sub-tree serially into its own list.  The
+// accepted boxes are disjoint, so the final (lo_j, lo_i) sort fixes one
+// order whatever the traversal -- the reference's order (regrid.py:182).
+static void cluster_task(const Prefix &F, const Prefix *BADp, double eff, Node nd,
+                         std::vector<std::vector<std::array<int, 4>>> &lists) {
+    if ((int64_t)(nd.i1 - nd.i0 + 1) * (nd.j1 - nd.j0 + 1) <= kTaskCells) {
+        std::vector<std::array<int, 4>> mine;
+        cluster_subtree(F, BADp, eff, nd, mine);
+#pragma omp critical(mlamr_cluster_lists)
+        lists.push_back(std::move(mine));
+        return;
+    }
+    std::vector<int64_t> sx, sy;
+    std::array<int, 4> bx;
+    Node l, r;
+    const int k = cluster_node(F, BADp, eff, nd, bx, l, r, sx, sy);
+    if (k == 1) {
+#pragma omp critical(mlamr_cluster_lists)
+        lists.push_back({bx});
+    } else if (k == 2) {
+#pragma omp task default(none) firstprivate(l, eff, BADp) shared(F, lists)
+        cluster_task(F, BADp, eff, l, lists);
+#pragma omp task default(none) firstprivate(r, eff, BADp) shared(F, lists)
+        cluster_task(F, BADp, eff, r, lists);
+    }
+}
+
+static int cluster_recursion(const Prefix &F, const Prefix *BADp, int ny, int nx, double eff,
+                             int32_t *out_boxes, int max_boxes) {
+    std::vector<std::vector<std::array<int, 4>>> lists;
+    if (ny > 0 && nx > 0) {
+        const Node root{0, 0, nx - 1, ny - 1};
+#pragma omp parallel default(none) shared(F, BADp, eff, root, lists)
+#pragma omp single
+        cluster_task(F, BADp, eff, root, lists);
+    }
+    std::vector<std::array<int, 4>> boxes;
+    for (auto &v : lists) boxes.insert(boxes.end(), v.begin(), v.end());
+    std::sort(boxes.begin(), boxes.end(), [](const std::array<int, 4> &a, const std::array<int, 4> &b) {
         return a[1] != b[1] ? a[1] < b[1] : a[0] < b[0];
     });
     if ((int)boxes.size() > max_boxes) return -1;

@@ -225,6 +225,36 @@ __global__ void __launch_bounds__(NTA) k_ghost_plan(mlamr_level lv, const int64_
     }
 }
 
+// Compacted list of the plan's interpolated cells (-1 entries): int32 pairs
+// (patch, ghost idx), appended with warp-aggregated atomics, the count in
+// *count.  The order is not deterministic, and need not be: every listed
+// cell is interpolated independently into its own location.  Keeps the
+// compaction on the device (no host round trip for the count).
+__global__ void __launch_bounds__(NTA) k_plan_interp_cells(mlamr_level lv, const int64_t *gbase,
+                                                           const int64_t *plan, const int32_t *patch_list,
+                                                           int n_rows, int32_t *cells, int32_t *count) {
+    const int row = grid_row();
+    if (row >= n_rows) return;
+    const int p = patch_list ? patch_list[row] : row;
+    const int32_t *b = lv.box + 4 * p;
+    const int nghost = 4 * (b[2] - b[0] + 1 + 2 * MLAMR_G) + 4 * (b[3] - b[1] + 1);
+    const int lane = threadIdx.x & 31;
+    for (int base = blockIdx.x * NTA; base < nghost; base += gridDim.x * NTA) {
+        const int idx = base + threadIdx.x;
+        const bool want = idx < nghost && plan[gbase[p] + idx] == -1;
+        const unsigned mask = __ballot_sync(0xffffffffu, want);
+        if (mask == 0u) continue;
+        const int leader = __ffs(mask) - 1;
+        int pos = 0;
+        if (lane == leader) pos = atomicAdd(count, __popc(mask));
+        pos = __shfl_sync(0xffffffffu, pos, leader) + __popc(mask & ((1u << lane) - 1u));
+        if (want) {
+            cells[2 * pos] = p;
+            cells[2 * pos + 1] = idx;
+        }
+    }
+}
+
 // sibling copies (ghost.py:186-196): one CTA of NTC threads per patch.  A
 // thread moves ghost cells in PAIRS -- consecutive plan entries are
 // neighbouring cells of a frame row (or the two cells of a side band on one
@@ -359,8 +389,10 @@ __global__ void __launch_bounds__(NTA) k_copy_pairs_of_plan(mlamr_level lv, cons
 template <int M>
 __global__ void __launch_bounds__(NTA) k_fill_interp(mlamr_level lv, mlamr_level par, const double *par_old,
                                                      double theta, int r_x, int r_y, const int32_t *cells,
-                                                     int n_cells, mlamr_params prm, const int32_t *status) {
+                                                     int n_cells, const int32_t *n_cells_dev, mlamr_params prm,
+                                                     const int32_t *status) {
     if (status != nullptr && *status != 0) return;
+    if (n_cells_dev != nullptr) n_cells = min(n_cells, *n_cells_dev);
     const double tol = prm.dry_tolerance;
     const int64_t FS = lv.field_stride;
     for (int c = blockIdx.x * NTA + threadIdx.x; c < n_cells; c += gridDim.x * NTA) {
@@ -1060,7 +1092,7 @@ extern "C" int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *pare
                                          double theta, int r_x, int r_y, const int32_t *bcs, mlamr_params prm,
                                          const int32_t *status, const int64_t *gbase, const int64_t *plan,
                                          const int32_t *patch_list, int n_list, int max_ghost,
-                                         const int32_t *interp_cells, int n_interp,
+                                         const int32_t *interp_cells, int n_interp, const int32_t *n_interp_dev,
                                          const int32_t *bc_patches, int n_bc, void *stream) {
     const int nb = patch_list ? n_list : lv.num_patches;
     cudaStream_t st = as_stream(stream);
@@ -1069,13 +1101,57 @@ extern "C" int mlamr_fill_ghosts_planned(mlamr_level lv, const mlamr_level *pare
         constexpr int M = decltype(Mc)::value;
         if (nb > 0) k_fill_copy<M><<<nb, NTC, 0, st>>>(lv, gbase, plan, patch_list, status);
         if (parent != nullptr && n_interp > 0) {
-            const int blocks = (int)std::min<int64_t>((n_interp + NTA - 1) / NTA, 148 * 32);
+            // with a device-side count n_interp is only a capacity: a
+            // grid-stride launch of at most 8 blocks per SM
+            const int cap = n_interp_dev ? 148 * 8 : 148 * 32;
+            const int blocks = (int)std::min<int64_t>((n_interp + NTA - 1) / NTA, cap);
             k_fill_interp<M><<<blocks, NTA, 0, st>>>(lv, *parent, parent_old_state, theta, r_x, r_y,
-                                                     interp_cells, n_interp, prm, status);
+                                                     interp_cells, n_interp, n_interp_dev, prm, status);
         }
         if (n_bc > 0) k_fill_bc<M><<<n_bc, NTA, 0, st>>>(lv, bc_patches, b, status);
     });
     if (rc) return rc;
+    return (int)cudaGetLastError();
+}
+
+// Column sums of per-block partials: one block per column, a fixed
+// thread-strided order and a fixed tree, so the result is deterministic.
+__global__ void __launch_bounds__(NTA) k_sum_partials(const double *part, long long rows, int cols, double scale,
+                                                      double *acc, double *acc2, int init) {
+    __shared__ double red[NTA];
+    const int c = blockIdx.x;
+    double v = 0.0;
+    for (long long r = threadIdx.x; r < rows; r += NTA) v = v + part[r * cols + c];
+    const double sm = block_sum<NTA>(v, red);
+    if (threadIdx.x == 0) {
+        const double sc = sm * scale;
+        acc[c] = init ? sc : acc[c] + sc;
+        if (acc2 != nullptr) acc2[c] = acc2[c] + sc;
+    }
+}
+
+extern "C" int mlamr_sum_partials(const double *part, long long rows, int cols, double scale, double *acc,
+                                  double *acc2, int init, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    if (cols <= 0) return 0;
+    if (rows <= 0) {
+        if (!init) return 0;
+        return (int)cudaMemsetAsync(acc, 0, sizeof(double) * cols, st);   // +0.0
+    }
+    k_sum_partials<<<cols, NTA, 0, st>>>(part, rows, cols, scale, acc, acc2, init);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_plan_interp_cells(mlamr_level lv, const int64_t *gbase, const int64_t *plan,
+                                       const int32_t *patch_list, int n_list, int max_ghost, int32_t *cells,
+                                       int32_t *count, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return (int)e;
+    const int nb = patch_list ? n_list : lv.num_patches;
+    if (nb <= 0) return 0;
+    const dim3 grid = row_grid((unsigned)std::max(1, std::min(16, (max_ghost + NTA - 1) / NTA)), nb);
+    k_plan_interp_cells<<<grid, NTA, 0, st>>>(lv, gbase, plan, patch_list, nb, cells, count);
     return (int)cudaGetLastError();
 }
 

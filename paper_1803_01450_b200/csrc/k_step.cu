@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(NTF) k_step_finalize(mlamr_level lv, const dou
                                                       double *__restrict__ dst,
                                                       const int32_t *__restrict__ tiles,
                                                       int n_tiles, double dt,
-                                                      const long long *speed_bits,
+                                                      long long *speed_bits,
                                                       const double *tile_acc, double *acc,
                                                       int32_t *status, int32_t *bad_patch,
-                                                      double *chunk, unsigned int *ticket) {
+                                                      double *chunk, unsigned int *ticket, int reset_speeds) {
     __shared__ double red[NTF];
     __shared__ int viol;
     __shared__ bool last;
@@ -155,7 +155,13 @@ __global__ void __launch_bounds__(NTF) k_step_finalize(mlamr_level lv, const dou
         ticket[1] = 0u;
     }
     __syncthreads();
-    if (!viol) return;
+    if (!viol) {
+        // every block has read the speeds (ticket): leave them at "all dry"
+        // for the next step's atomicMax (replaces a fill before each step)
+        if (reset_speeds)
+            for (int p = t; p < lv.num_patches; p += NTF) speed_bits[p] = -1LL;
+        return;
+    }
     // restore every violating patch's interior (the reference raises before
     // touching it, physics.py:342-347)
     const int64_t FS = lv.field_stride;
@@ -234,9 +240,9 @@ extern "C" int mlamr_step(mlamr_level lv, const double *src_state, double *dst_s
 
 extern "C" int mlamr_step_finalize(mlamr_level lv, const double *src_state, double *dst_state,
                                    const int32_t *tiles, int n_tiles, double dt,
-                                   mlamr_params prm, const long long *speed_bits,
+                                   mlamr_params prm, long long *speed_bits,
                                    const double *tile_acc, double *acc, int32_t *status,
-                                   int32_t *bad_patch, void *stream) {
+                                   int32_t *bad_patch, int reset_speeds, void *stream) {
     cudaStream_t st = as_stream(stream);
     // scratch for the chunk sums and the completion ticket, one per
     // (device, stream): launches on one stream are ordered, so reuse is safe
@@ -261,9 +267,9 @@ extern "C" int mlamr_step_finalize(mlamr_level lv, const double *src_state, doub
     double *chunk = sc.chunk;
     unsigned int *ticket = sc.ticket;
     switch (prm.num_layers) {
-        case 1: k_step_finalize<1><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
-        case 2: k_step_finalize<2><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
-        case 3: k_step_finalize<3><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket); break;
+        case 1: k_step_finalize<1><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket, reset_speeds); break;
+        case 2: k_step_finalize<2><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket, reset_speeds); break;
+        case 3: k_step_finalize<3><<<FIN_BLOCKS, NTF, 0, st>>>(lv, src_state, dst_state, tiles, n_tiles, dt, speed_bits, tile_acc, acc, status, bad_patch, chunk, ticket, reset_speeds); break;
         default: return -1;
     }
     return (int)cudaGetLastError();

@@ -436,7 +436,7 @@ int mlamr_pt_fill_ghosts(mlamr_pt *pt, int level, double t) {
         }
     }
     return mlamr_fill_ghosts_planned(lv, pp, old, theta, rx, ry, pt->bcs, pt->prm, pt->status.p, L->gbase.p,
-                                     L->plan.p, nullptr, 0, L->max_ghost, L->interp.p, pp ? L->n_interp : 0,
+                                     L->plan.p, nullptr, 0, L->max_ghost, L->interp.p, pp ? L->n_interp : 0, nullptr,
                                      L->bcp.p, L->n_bc, pt->st);
 }
 
@@ -454,7 +454,7 @@ int mlamr_pt_step_level(mlamr_pt *pt, int level, double dt, int y_first, double 
     rc |= mlamr_step(lv, src, dst, L->tiles.p, L->n_tiles, L->tile_tx, dt, y_first, pt->prm, L->speed.p,
                      L->tile_acc.p, pt->status.p, nullptr, nullptr, pt->st);
     rc |= mlamr_step_finalize(lv, src, dst, L->tiles.p, L->n_tiles, dt, pt->prm, L->speed.p, L->tile_acc.p,
-                              pt->acc.p, pt->status.p, pt->bad.p, pt->st);
+                              pt->acc.p, pt->status.p, pt->bad.p, 0, pt->st);
     if (rc) return rc;
     double acc[MLAMR_MAX_LAYERS + 2];
     int32_t bad = 0;

@@ -361,14 +361,20 @@ class LevelPool:
             plan = torch.empty(max(total, 1), dtype=torch.int64, device=self.device)
             N.check(N.lib().mlamr_ghost_plan(self.struct(), gbase_d.data_ptr(), plan.data_ptr(), int(ng.max()),
                                              self.stream.cuda_stream), "ghost_plan")
-            sel = plan[:total] == -1
+            # interpolated cells (-1) compacted on the device: no host
+            # round trip for their count (n_cells is the list's capacity)
+            cap = max(total, 1)
+            cells = torch.empty(2 * cap, dtype=torch.int32, device=self.device)
+            count = torch.zeros(1, dtype=torch.int32, device=self.device)
             if self.owned is not None:
-                own_cells = torch.repeat_interleave(torch.from_numpy(self.owned).to(self.device),
-                                                    torch.from_numpy(ng).to(self.device))
-                sel &= own_cells
-            gidx = torch.nonzero(sel).flatten()
-            patch = torch.searchsorted(gbase_d, gidx, right=True) - 1
-            cells = torch.stack([patch, gidx - gbase_d[patch]], dim=1).to(torch.int32).contiguous()
+                pl, nl = (self.owned_d.data_ptr(), self.n_owned) if self.n_owned else (None, 0)
+            else:
+                pl, nl = None, self.P
+            if nl:
+                N.check(N.lib().mlamr_plan_interp_cells(self.struct(), gbase_d.data_ptr(), plan.data_ptr(), pl,
+                                                        nl, int(ng.max()), cells.data_ptr(), count.data_ptr(),
+                                                        self.stream.cuda_stream), "plan_interp_cells")
+            self.interp_count = count
         s = self.spec
         touch = (b[:, 0] == 0) | (b[:, 2] == s.nx - 1) | (b[:, 1] == 0) | (b[:, 3] == s.ny - 1)
         if self.owned is not None:
@@ -376,7 +382,7 @@ class LevelPool:
         bcp = np.flatnonzero(touch).astype(np.int32)
         bc_d = A.upload(bcp, self.device, self.stream) if len(bcp) else torch.zeros(1, dtype=torch.int32,
                                                                                      device=self.device)
-        self._plan = (gbase_d, plan, cells, int(cells.shape[0]), bc_d, len(bcp), int(ng.max()) if len(ng) else 0)
+        self._plan = (gbase_d, plan, cells, cap if nl else 0, bc_d, len(bcp), int(ng.max()) if len(ng) else 0)
         return self._plan
 
     def coarse_base(self, rx: int, ry: int):

@@ -160,6 +160,7 @@ class Simulation:
             self.bad = torch.full((1,), 2 ** 31 - 1, dtype=torch.int32, device=self.dev)
             self.acc = torch.zeros(M + 2, dtype=torch.float64, device=self.dev)
             self.delta_acc = torch.zeros(3, M, dtype=torch.float64, device=self.dev)  # refine, derefine, event
+            self._mass_d = torch.zeros(M, dtype=torch.float64, device=self.dev)
             # whole-level bathymetry (the scenario's fill_bathymetry source):
             # async copies from pinned host staging kept on the problem
             self.level_bathy = [b.to(self.dev, non_blocking=True) for b in _pinned_bathy(problem)]
@@ -168,6 +169,12 @@ class Simulation:
             self._wave_tol = torch.tensor(list(problem.wave_tolerance), dtype=torch.float64, device=self.dev)
         self._flagbuf = {}
         self._scratch_bufs = {}
+        self._pinned_bufs = {}
+        # the step's per-patch observed speeds are reset to -1 by its
+        # finalize; True keeps them readable after the step (tests)
+        self.keep_step_speeds = False
+        self._speed_cache = None   # (state key, level-1 speed bits) from _step_readback
+        self._restores = 0
         # childless levels: sibling ghost copy inside the step's staging
         # (mlamr_step with a ghost plan; the finite check then reads those
         # cells through the plan too).  On C4 it drops the 0.29 ms sibling
@@ -271,10 +278,14 @@ class Simulation:
             raise_status(st, where)
 
     # -- mass accounting and finite check (driver.py:138-153, 286-297) ---------
-    def _level_reduce(self, level: int) -> torch.Tensor:
+    def _level_reduce(self, level: int, tot: torch.Tensor, init: bool) -> None:
+        """Adds this level's composite volume per layer into ``tot`` (or
+        sets it, ``init``) and runs the finite check (status)."""
         pool = self.levels[level]
         if pool.P == 0:
-            return torch.zeros(self.M, dtype=torch.float64, device=self.dev)
+            if init:
+                self._call(self.lib.mlamr_sum_partials, None, 0, self.M, 1.0, tot.data_ptr(), None, 1, self.sh)
+            return
         # a few blocks per patch, each thread over ~8 cells: the per-block
         # reduction, not the bytes, had dominated with one cell per thread
         bpp = max(1, min(64, -(-pool.max_cells // (8 * 256))))
@@ -291,18 +302,36 @@ class Simulation:
                        ghosts.data_ptr(), child, part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, gb, gp,
                        self.sh)
             s = self.spec(level)
-            return part.view(-1, self.M).sum(dim=0) * (s.dx * s.dy)
+            self._call(self.lib.mlamr_sum_partials, part.data_ptr(), pool.P * bpp, self.M, s.dx * s.dy,
+                       tot.data_ptr(), None, int(init), self.sh)
+
+    def _mass_device(self) -> torch.Tensor:
+        """Composite volume per layer on the device (driver.py:138-153)."""
+        tot = self._mass_d
+        first = True
+        for lev in range(1, self.L + 1):
+            if lev in self.levels:
+                self._level_reduce(lev, tot, first)
+                first = False
+        return tot
+
+    def _pinned(self, name: str, n: int, dtype) -> torch.Tensor:
+        key = (name, dtype)
+        buf = self._pinned_bufs.get(key)
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(2 * n, 64), dtype=dtype, pin_memory=True)
+            self._pinned_bufs[key] = buf
+        return buf[:n]
 
     def composite_mass(self) -> np.ndarray:
         with torch.cuda.stream(self.stream):
-            tot = torch.zeros(self.M, dtype=torch.float64, device=self.dev)
-            for lev in range(1, self.L + 1):
-                if lev in self.levels:
-                    tot = tot + self._level_reduce(lev)
+            tot = self._mass_device()
+            out = self._pinned("mass", self.M, torch.float64)
+            out.copy_(tot, non_blocking=True)
         self.stream.synchronize()
         arena().reset()
         self.d2h_bytes += 8 * self.M
-        return tot.cpu().numpy()
+        return out.numpy().copy()
 
     # -- ghost filling (driver.py:157-190) ------------------------------------
     def fill_level_ghosts(self, level: int, t: float, siblings: bool = True) -> None:
@@ -344,7 +373,7 @@ class Simulation:
             pl, nl = bc_d.data_ptr(), n_bc
         self._call(self.lib.mlamr_fill_ghosts_planned, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
                    self.prm, self.status.data_ptr(), gbase.data_ptr(), plan.data_ptr(), pl, nl, max_ghost,
-                   cells.data_ptr(), n_cells, bc_d.data_ptr(), n_bc, self.sh)
+                   cells.data_ptr(), n_cells, pool.interp_count.data_ptr(), bc_d.data_ptr(), n_bc, self.sh)
         pool.ghosts_in_cur = True
 
     # -- regridding (driver.py:192-222, regrid.py:235-353) -------------------------
@@ -556,7 +585,7 @@ class Simulation:
                 self._call(self.lib.mlamr_regrid_fill, new.struct(), ol, par.struct(), rx, ry, self.prm,
                            part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
                 if not init:
-                    self.delta_acc[0] += part.view(-1, M).sum(dim=0)
+                    self._add_delta(0, part, new.P * bpp)
             new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
             if old is not None and old.P and not init:
                 bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
@@ -564,7 +593,7 @@ class Simulation:
                 pl, nl = old.work_list()
                 self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
                            rx, ry, self.prm, part.data_ptr(), bpp, pl, nl, self.sh)
-                self.delta_acc[1] += part.view(-1, M).sum(dim=0)
+                self._add_delta(1, part, old.P * bpp)
         self.host_prof["regrid.fill+derefine"] += time.perf_counter() - tq
         tq = time.perf_counter()
         new.ghosts_in_cur = False
@@ -597,8 +626,8 @@ class Simulation:
         if pool.P == 0:
             return
         y_first = int(self.steps[level] % 2)
-        with torch.cuda.stream(self.stream):
-            pool.speed_bits.fill_(-1)
+        # speed_bits are at "all dry" (-1) here: set at pool creation, and
+        # reset by the previous finalize (reset_speeds) or level_speed
         src, dst = pool.state, pool.other
         lv = pool.struct(src)
         if _LOG_STEP_BYTES:
@@ -624,7 +653,8 @@ class Simulation:
             self.step_events.append((e0, e1, pool))
         self._call(self.lib.mlamr_step_finalize, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
                    pool.n_tiles, dt, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
-                   self.acc.data_ptr(), self.status.data_ptr(), self.bad.data_ptr(), self.sh)
+                   self.acc.data_ptr(), self.status.data_ptr(), self.bad.data_ptr(), int(not self.keep_step_speeds),
+                   self.sh)
         pool.cur = 1 - pool.cur
         pool.ghosts_in_cur = False
         self.stats.total_cell_updates += pool.ncells
@@ -669,17 +699,33 @@ class Simulation:
             del self._stash[level]
 
     # -- coarse step (driver.py:299-362) ----------------------------------------------
+    def _speed_key(self, level: int):
+        pool = self.levels.get(level)
+        return (id(pool), pool.cur if pool is not None else -1, int(self.steps[level]), self._restores)
+
+    def _enqueue_speed(self, pool) -> torch.Tensor:
+        """k_max_speed over a level and the copy of its per-patch speed bits
+        to pinned memory (read after the next synchronisation)."""
+        self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(), pool.tiles_d.data_ptr(),
+                   pool.n_tiles, pool.tile_tx, self.prm, pool.speed_bits.data_ptr(), self.sh)
+        with torch.cuda.stream(self.stream):
+            bits_h = self._pinned("speed", pool.P, torch.int64)
+            bits_h.copy_(pool.speed_bits[:pool.P], non_blocking=True)
+            pool.speed_bits.fill_(-1)   # back to "all dry" for the next step
+        return bits_h
+
     def level_speed(self, level: int) -> float:
         pool = self.levels.get(level)
         if pool is None or pool.P == 0:
             return 0.0
-        with torch.cuda.stream(self.stream):
-            pool.speed_bits.fill_(-1)
-        self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(), pool.tiles_d.data_ptr(),
-                   pool.n_tiles, pool.tile_tx, self.prm, pool.speed_bits.data_ptr(), self.sh)
-        self.stream.synchronize()
-        self.d2h_bytes += 8 * pool.P
-        bits = pool.speed_bits[:pool.P].cpu().numpy()
+        cache = self._speed_cache
+        if level == 1 and cache is not None and cache[0] == self._speed_key(1):
+            bits = cache[1]   # read back with the previous step's mass
+        else:
+            bits_h = self._enqueue_speed(pool)
+            self.stream.synchronize()
+            self.d2h_bytes += 8 * pool.P
+            bits = bits_h.numpy()
         sp = np.where(bits < 0, 0, bits).view(np.float64)
         return sp
 
@@ -710,22 +756,21 @@ class Simulation:
             self.specs[lev - 1] = replace(s, r_t=rt)
             dtl = dtl / rt
 
+    def _add_delta(self, k: int, part: torch.Tensor, rows: int) -> None:
+        """delta_acc[k] (0 refine, 1 derefine) and this coarse step's event
+        delta (delta_acc[2]) += the column sums of a kernel's partials."""
+        self._call(self.lib.mlamr_sum_partials, part.data_ptr(), rows, self.M, 1.0, self.delta_acc[k].data_ptr(),
+                   self.delta_acc[2].data_ptr(), 0, self.sh)
+
     def advance_coarse_step(self, dt: float) -> None:
-        with torch.cuda.stream(self.stream):
-            self.delta_acc[2].zero_()
-            before = self.delta_acc[:2].sum(dim=0).clone()
+        self._call(self.lib.mlamr_sum_partials, None, 0, self.M, 1.0, self.delta_acc[2].data_ptr(), None, 1,
+                   self.sh)
         with self._timed("advance(host enqueue)"):
             self.advance_level(1, dt, self.time)
         self.time += dt
-        with self._timed("sync(wait for device)"):
-            self._sync_status(f"at t={self.time:.6g}")
-        with self._timed("mass+finite"):
-            mass = self.composite_mass()
-        with torch.cuda.stream(self.stream):
-            ev = self.delta_acc[:2].sum(dim=0) - before
-            self._reduce_event(ev)
-            event = ev.cpu().numpy()   # ordered after ev on the driver stream
-        self.d2h_bytes += 8 * self.M
+        where = f"at t={self.time:.6g}"
+        with self._timed("sync+mass+finite"):
+            mass, event, nonfinite = self._step_readback(where)
         sync = mass - self._mass_prev - event
         if not self.stats.sync_delta:
             self.stats.sync_delta = [0.0] * self.M
@@ -733,7 +778,47 @@ class Simulation:
             self.stats.sync_delta[m] += float(sync[m])
         self._mass_prev = mass
         self.stats.num_coarse_steps += 1
-        self._sync_status(f"at t={self.time:.6g}")
+        if nonfinite:
+            # the reference counts the step, then checks finiteness (driver.py:299-309)
+            raise_status(N.ST_NONFINITE, where)
+
+    def _step_readback(self, where: str):
+        """End of a coarse step with ONE host synchronisation: the composite
+        mass and finite check (driver.py:286-297), this step's event delta,
+        the status word, and -- for the next choose_dt -- level 1's observed
+        speeds are enqueued and copied to pinned memory together; then the
+        status is raised as the reference would: the advance's own errors
+        here, a non-finite state (returned as a flag) by the caller after
+        the step is counted."""
+        M = self.M
+        pool1 = self.levels.get(1)
+        pre = pool1 is not None and pool1.P > 0
+        with torch.cuda.stream(self.stream):
+            tot = self._mass_device()
+            self._reduce_event(self.delta_acc[2])
+            hb = self._pinned("readback", 2 * M, torch.float64)
+            hb[:M].copy_(tot, non_blocking=True)
+            hb[M:].copy_(self.delta_acc[2], non_blocking=True)
+            hs = self._pinned("status", 2, torch.int32)
+            hs[:1].copy_(self.status, non_blocking=True)
+            hs[1:].copy_(self.bad, non_blocking=True)
+            if pre:
+                bits_h = self._enqueue_speed(pool1)
+        self.stream.synchronize()
+        arena().reset()
+        self.d2h_bytes += 16 * M + 8
+        st = int(hs[0])
+        nonfinite = bool(st & N.ST_NONFINITE)
+        st &= ~N.ST_NONFINITE
+        if st:
+            self._speed_cache = None
+            if st & N.ST_CFL:
+                raise CflViolationError(f"Courant number > 1 on patch {int(hs[1])} {where}")
+            raise_status(st, where)
+        if pre and not nonfinite:
+            self.d2h_bytes += 8 * pool1.P
+            self._speed_cache = (self._speed_key(1), bits_h.numpy().copy())
+        return hb[:M].numpy().copy(), hb[M:].numpy().copy(), nonfinite
 
     def _reduce_event(self, ev: torch.Tensor) -> None:
         """Single GPU: the refine/derefine delta of this coarse step is
@@ -882,6 +967,8 @@ class Simulation:
         return self.levels[lev].boxes
 
     def _restore_from(self, snap: dict) -> None:
+        self._speed_cache = None
+        self._restores += 1
         self.time = snap["time"]
         self.steps = dict(snap["steps"])
         self.specs = list(snap["specs"])

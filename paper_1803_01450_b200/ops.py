@@ -126,7 +126,7 @@ def step_patch(patch, dt: float, params, y_first: bool = False) -> StepResult:
                          status.data_ptr(), None, None, sh), "step")
     N.check(L.mlamr_step_finalize(lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(), pool.n_tiles,
                                   dt, prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
-                                  acc.data_ptr(), status.data_ptr(), bad.data_ptr(), sh), "finalize")
+                                  acc.data_ptr(), status.data_ptr(), bad.data_ptr(), 0, sh), "finalize")
     st = int(status.item())
     bits = int(pool.speed_bits[0].item())
     speed = 0.0 if bits < 0 else float(np.array([bits], np.int64).view(np.float64)[0])

@@ -24,7 +24,9 @@ def cluster_boxes(flags: np.ndarray, efficiency_target: float, allowed=None) -> 
     f = np.ascontiguousarray(flags, dtype=np.uint8)
     ny, nx = f.shape
     a = None if allowed is None else np.ascontiguousarray(allowed, dtype=np.uint8)
-    cap = 4096
+    # every box holds a flagged cell: ny*nx boxes always fit (np.empty only
+    # commits the pages that get written)
+    cap = max(ny * nx, 1)
     while True:
         out = np.empty((cap, 4), dtype=np.int32)
         n = N.lib().mlamr_cluster_flags(f.ctypes.data, ny, nx, float(efficiency_target),
@@ -69,7 +71,7 @@ def cluster_boxes_device(flags_d, allowed_d, ny: int, nx: int, efficiency_target
 
 
 def _cluster_from_sat(hf, hb, ny, nx, efficiency_target):
-    cap = 4096
+    cap = max(ny * nx, 1)   # one pass (see cluster_boxes)
     while True:
         out = np.empty((cap, 4), dtype=np.int32)
         n = N.lib().mlamr_cluster_sat(hf.data_ptr(), hb.data_ptr(), ny, nx, float(efficiency_target),

@@ -276,12 +276,26 @@ class ShardedSimulation(Simulation):
             self.comm.allreduce(self.bad, dist.ReduceOp.MIN if self.world > 1 else None)
         super()._sync_status(where)
 
+    def _step_readback(self, where: str):
+        """Status, mass and event delta all-reduced over the ranks (the
+        single-GPU readback batches them into one synchronisation)."""
+        self._sync_status(where)
+        mass = self.composite_mass()
+        with torch.cuda.stream(self.stream):
+            ev = self.delta_acc[2].clone()
+            self._reduce_event(ev)
+        self.stream.synchronize()
+        self.d2h_bytes += 8 * self.M
+        event = ev.cpu().numpy()
+        with torch.cuda.stream(self.stream):
+            self.comm.allreduce(self.status, dist.ReduceOp.MAX if self.world > 1 else None)
+        self.stream.synchronize()
+        nonfinite = bool(int(self.status.item()) & N.ST_NONFINITE)
+        return mass, event, nonfinite
+
     def composite_mass(self) -> np.ndarray:
         with torch.cuda.stream(self.stream):
-            tot = torch.zeros(self.M, dtype=torch.float64, device=self.dev)
-            for lev in range(1, self.L + 1):
-                if lev in self.levels:
-                    tot = tot + self._level_reduce(lev)
+            tot = self._mass_device().clone()
             self.comm.allreduce(tot)
         self.stream.synchronize()
         from .device import arena
@@ -300,6 +314,7 @@ class ShardedSimulation(Simulation):
                                pool.speed_bits.data_ptr(),
                                self.sh)
                 best = torch.max(pool.speed_bits[:pool.P]).reshape(1)
+                pool.speed_bits.fill_(-1)   # back to "all dry" for the next step (see the driver)
             self.comm.allreduce(best, dist.ReduceOp.MAX if self.world > 1 else None)
         self.stream.synchronize()
         b = int(best.item())
@@ -424,7 +439,7 @@ class ShardedSimulation(Simulation):
                     self._call(self.lib.mlamr_regrid_fill, new.struct(), ol, par.struct(), rx, ry, self.prm,
                                part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
                 if not init:
-                    self.delta_acc[0] += part.view(-1, M).sum(dim=0)
+                    self._add_delta(0, part, new.P * bpp)
             new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
             if old is not None and old.P and not init:
                 bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
@@ -433,7 +448,7 @@ class ShardedSimulation(Simulation):
                 if nl > 0:
                     self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
                                rx, ry, self.prm, part.data_ptr(), bpp, pl, nl, self.sh)
-                self.delta_acc[1] += part.view(-1, M).sum(dim=0)
+                self._add_delta(1, part, old.P * bpp)
         # (d) install and fill the new shadows from their owners
         self.layout[level + 1] = nboxes
         self.owner[level + 1] = new_owner

@@ -154,6 +154,7 @@ def test_step_speed_is_nan_when_a_velocity_is_nan():
     from paper_1803_01450_b200 import problems
     from paper_1803_01450_b200.driver import Simulation
     sim = Simulation(problems.config2(n_coarse_steps=1))
+    sim.keep_step_speeds = True   # read the step's speeds afterwards
     lev = sim.L
     pool = sim.levels[lev]
     assert pool.P > 1
