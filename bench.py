@@ -99,6 +99,62 @@ def coarse_step(sim):
     sim.advance_coarse_step(dt)
 
 
+def kernel_rooflines(timer, peak, span_s):
+    """Per-kernel roofline of the auxiliary kernels timed in the region:
+    algorithmic bytes (driver.py's _kt1 call sites) over
+    the CUDA-event launch durations, against the HBM peak."""
+    out = []
+    for name, evs in sorted((timer or {}).items()):
+        durs = [a.elapsed_time(b) * 1e-3 for a, b, _ in evs]
+        byts = [int(n() if callable(n) else n) for _, _, n in evs]
+        if not durs or sum(durs) <= 0:
+            continue
+        gbs = sum(byts) / sum(durs) / 1e9
+        out.append({"kernel": name, "launches": len(durs), "avg_launch_ms": 1e3 * sum(durs) / len(durs),
+                    "bytes_per_launch": int(sum(byts) / len(byts)), "achieved_gbs": gbs,
+                    "frac": gbs / peak, "share_of_step": sum(durs) / span_s})
+    return out
+
+
+def stress_run(stream, steps: int, warmup: int, peak):
+    """C5s (problems.config5_stress): C5 with Bernoulli(0.05) flags, so the
+    level-2 layout is rebuilt -- refine, copy, derefine -- every coarse step.
+    Device-timed like the main line; reported inside it."""
+    import torch
+    from paper_1803_01450_b200 import problems
+    from paper_1803_01450_b200.driver import Simulation
+    pb = problems.config5_stress()
+    sim = Simulation(pb, stream=stream)
+    for _ in range(warmup):
+        coarse_step(sim)
+    sim.kernel_timer = {}
+    sim.step_timer_level = sim.L
+    sim.step_events = []
+    r0, c0 = sim.stats.num_regrids, sim.stats.total_cell_updates
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        coarse_step(sim)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    cells = (sim.stats.total_cell_updates - c0) * pb.num_layers
+    durs = [a.elapsed_time(b) * 1e-3 for a, b, _ in sim.step_events]
+    byts = [step_bytes(p, pb.num_layers) for _, _, p in sim.step_events]
+    res = {"workload": "C5s: C5 (L1 1280^2, r=(4,2), 16x16 patches, dynamic r_t) with Bernoulli(0.05) flags",
+           "value": cells / (ms * 1e-3), "unit": UNIT, "steps": steps, "warmup": warmup,
+           "ms_per_step": ms / steps, "regrids_per_step": (sim.stats.num_regrids - r0) / steps,
+           "patches_level2": int(sim.levels[2].P) if 2 in sim.levels else 0,
+           "step_kernel": {"avg_launch_ms": 1e3 * float(sum(durs) / len(durs)) if durs else None,
+                           "achieved_gbs": sum(byts) / sum(durs) / 1e9 if durs else None,
+                           "share_of_step": sum(durs) / (ms * 1e-3) if durs else None},
+           "kernels": kernel_rooflines(sim.kernel_timer, peak, ms * 1e-3)}
+    sim.close()
+    return res
+
+
 def step_bytes(pool, M):
     """Algorithmic HBM bytes of one step launch on a level:
     8*[(3M+1)*(nx+2)(ny+2) + 3M*nx*ny] per stepped (owned) patch."""
@@ -205,6 +261,7 @@ def b200_arm(args):
     _D.POOL_PROF.clear()
     sim.step_timer_level = L
     sim.step_events = []
+    sim.kernel_timer = {}
     launches0 = N.LAUNCHES[0]
     cells0 = sim.stats.total_cell_updates
     xbytes0 = getattr(sim, "bytes_exchanged", 0)
@@ -262,12 +319,22 @@ def b200_arm(args):
     achieved = (sum(byts) / sum(durs)) / 1e9 if durs else None
     step_share = sum(durs) / (ms * 1e-3) if durs else None
     sim.step_timer_level = None
+    kernels = kernel_rooflines(sim.kernel_timer, peak, ms * 1e-3)
+    sim.kernel_timer = None
     pool_bytes = sum(p.state.numel() * 8 * 2 + p.bathy.numel() * 8 for p in sim.levels.values())
     patches_per_level = ({str(k): int(len(v)) for k, v in sim.layout.items()}
                          if world > 1 else {str(k): v.P for k, v in sim.levels.items()})
     cells_per_level = {str(k): v.ncells for k, v in sim.levels.items()}
     host_ms = {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}
     xbytes = int((getattr(sim, "bytes_exchanged", 0) - xbytes0) / args.steps)
+
+    # ---- regrid stress (C5s), single GPU --------------------------------------
+    stress = None
+    if world == 1 and not args.no_stress and args.config == "C4":
+        # C5s's dynamic-r_t harness rule meets the CFL guard in its 4th coarse
+        # step (t = 19.17; the pre-change tree does the same): warm-up 1 + 2
+        # timed steps, each with a level-2 rebuild
+        stress = stress_run(stream, 2, 1, peak)
 
     # ---- e2e: host buffers -> device -> K steps -> host ---------------------
     e2e = None
@@ -344,6 +411,8 @@ def b200_arm(args):
                          "bytes_per_launch": int(np.mean(byts)) if byts else None,
                          "avg_launch_ms": 1e3 * float(np.mean(durs)) if durs else None,
                          "share_of_step": step_share, "peak_source": peak_kind},
+            "kernels_roofline": kernels,
+            "regrid_stress": stress,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": clk.summary(),
@@ -364,6 +433,7 @@ def main():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-stress", action="store_true", help="skip the C5s regrid-stress measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

@@ -702,21 +702,42 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
     // old-patch copies (regrid.py:311-323) one fine cell per thread, so a
     // warp moves contiguous row segments; old patches are ratio-aligned, so
     // a coarse cell's fine block lies in one old patch and the owner of the
-    // fine cell is the owner the refine pass below tests
-    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < nv.nx * nv.ny; idx += gridDim.x * NTA) {
-        const int j = idx / nv.nx, i = idx - (idx / nv.nx) * nv.nx;
-        const int fi = nv.lo_i + i, fj = nv.lo_j + j;
-        const int o = owner_at(ol.own, ol.level_nx, ol.level_ny, fi, fj);
-        if (o < 0) continue;
-        const int32_t *b = ol.box + 4 * o;
-        const int ONX = b[2] - b[0] + 1 + 2 * MLAMR_G;
-        const int64_t ks = ol.offset[o] + (int64_t)(fj - b[1] + MLAMR_G) * ONX + (fi - b[0] + MLAMR_G);
-        const int64_t kd = nv.off + (int64_t)(j + MLAMR_G) * nv.NX + (i + MLAMR_G);
-        double v[3 * M];
+    // fine cell is the owner the refine pass below tests.  RG cells per
+    // thread per round, each stage (owner lookups, source loads, stores)
+    // issued for all of them before the next: the copy is a chain of
+    // dependent loads (owner map -> old patch box/offset -> state), and
+    // independent cells in flight are what reaches the bandwidth.
+    constexpr int RG = 4;
+    const int ncell = nv.nx * nv.ny;
+    const int stride = gridDim.x * NTA;
+    for (int base = blockIdx.x * NTA + threadIdx.x; base < ncell; base += RG * stride) {
+        int64_t ks[RG], kd[RG];
 #pragma unroll
-        for (int f = 0; f < 3 * M; ++f) v[f] = ol.state[f * OF + ks];
+        for (int u = 0; u < RG; ++u) {
+            const int idx = base + u * stride;
+            ks[u] = -1;
+            kd[u] = 0;
+            if (idx >= ncell) continue;
+            const int j = idx / nv.nx, i = idx - (idx / nv.nx) * nv.nx;
+            const int fi = nv.lo_i + i, fj = nv.lo_j + j;
+            const int o = owner_at(ol.own, ol.level_nx, ol.level_ny, fi, fj);
+            if (o < 0) continue;
+            const int32_t *b = ol.box + 4 * o;
+            const int ONX = b[2] - b[0] + 1 + 2 * MLAMR_G;
+            ks[u] = ol.offset[o] + (int64_t)(fj - b[1] + MLAMR_G) * ONX + (fi - b[0] + MLAMR_G);
+            kd[u] = nv.off + (int64_t)(j + MLAMR_G) * nv.NX + (i + MLAMR_G);
+        }
+        double v[RG][3 * M];
 #pragma unroll
-        for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + kd] = v[f];
+        for (int u = 0; u < RG; ++u)
+            if (ks[u] >= 0)
+#pragma unroll
+                for (int f = 0; f < 3 * M; ++f) v[u][f] = ol.state[f * OF + ks[u]];
+#pragma unroll
+        for (int u = 0; u < RG; ++u)
+            if (ks[u] >= 0)
+#pragma unroll
+                for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + kd[u]] = v[u][f];
     }
     for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
         const int J = idx / cnx, I = idx % cnx;

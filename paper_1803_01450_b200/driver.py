@@ -87,6 +87,35 @@ class RunStats:
             f.write("\n")
 
 
+def regrid_fill_bytes(new_boxes, old_boxes, rx: int, ry: int, M: int) -> int:
+    """Algorithmic bytes of one k_regrid_fill launch (SURVEY.md §8(d) K3 +
+    K5): 8*(3M + 1 + (3M+1)/(r_x r_y)) per refined fine cell (written state,
+    read bathymetry, the parent stencil amortised over its children) and
+    8*6M per cell copied from an old patch.  Both box sets are
+    ratio-aligned, so the overlap is counted on the coarse grid."""
+    nb = np.asarray(new_boxes, np.int64).reshape(-1, 4)
+    ob = np.asarray(old_boxes, np.int64).reshape(-1, 4)
+    total = int(((nb[:, 2] - nb[:, 0] + 1) * (nb[:, 3] - nb[:, 1] + 1)).sum())
+    copied = 0
+    if len(ob) and len(nb):
+        c_new = np.stack([nb[:, 0] // rx, nb[:, 1] // ry, (nb[:, 2] + 1) // rx, (nb[:, 3] + 1) // ry], 1)
+        c_old = np.stack([ob[:, 0] // rx, ob[:, 1] // ry, (ob[:, 2] + 1) // rx, (ob[:, 3] + 1) // ry], 1)
+        W = int(max(c_new[:, 2].max(), c_old[:, 2].max())) + 1
+        H = int(max(c_new[:, 3].max(), c_old[:, 3].max())) + 1
+        d = np.zeros((H + 1, W + 1), np.int32)
+        np.add.at(d, (c_old[:, 1], c_old[:, 0]), 1)
+        np.add.at(d, (c_old[:, 1], c_old[:, 2]), -1)
+        np.add.at(d, (c_old[:, 3], c_old[:, 0]), -1)
+        np.add.at(d, (c_old[:, 3], c_old[:, 2]), 1)
+        cov = (np.cumsum(np.cumsum(d, 0), 1) > 0).astype(np.int64)
+        sat = np.zeros((H + 2, W + 2), np.int64)
+        sat[1:, 1:] = np.cumsum(np.cumsum(cov, 0), 1)
+        x0, y0, x1, y1 = c_new.T
+        copied = int((sat[y1, x1] - sat[y0, x1] - sat[y1, x0] + sat[y0, x0]).sum()) * rx * ry
+    refined = total - copied
+    return int(8 * (3 * M + 1 + (3 * M + 1) / (rx * ry)) * refined + 8 * 6 * M * copied)
+
+
 def _pinned_bathy(problem) -> list:
     """The problem's per-level bathymetry arrays staged once in pinned host
     memory (cached on the problem object, keyed by the arrays' identity), so
@@ -173,6 +202,8 @@ class Simulation:
         # the step's per-patch observed speeds are reset to -1 by its
         # finalize; True keeps them readable after the step (tests)
         self.keep_step_speeds = False
+        # {name: [(start event, end event, algorithmic bytes)]} when not None
+        self.kernel_timer = None
         self._speed_cache = None   # (state key, level-1 speed bits) from _step_readback
         self._restores = 0
         # childless levels: sibling ghost copy inside the step's staging
@@ -225,6 +256,24 @@ class Simulation:
     def _call(self, fn, *args, what=""):
         self.launches += 1
         N.check(fn(*args), what or fn.__name__)
+
+    # -- per-kernel timing for the bench (CUDA events on the driver stream) ------
+    def _kt0(self):
+        """Start event of a timed launch, or None when timing is off."""
+        if self.kernel_timer is None:
+            return None
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(self.stream)
+        return e
+
+    def _kt1(self, name: str, e0, nbytes) -> None:
+        """End of a timed launch: ``nbytes`` (int or a callable evaluated
+        after the timed region) = its algorithmic HBM bytes."""
+        if e0 is None:
+            return
+        e1 = torch.cuda.Event(enable_timing=True)
+        e1.record(self.stream)
+        self.kernel_timer.setdefault(name, []).append((e0, e1, nbytes))
 
     def _new_pool(self, level: int, boxes: np.ndarray) -> LevelPool:
         pool = LevelPool(self.spec(level), boxes, self.M, self.dev, self.stream, need_gown=level < self.L)
@@ -298,9 +347,12 @@ class Simulation:
             if getattr(pool, "fused_frame", False) and not pool.ghosts_in_cur:
                 gbase, plan = pool.ghost_plan()[:2]
                 gb, gp = gbase.data_ptr(), plan.data_ptr()
+            e0 = self._kt0()
             self._call(self.lib.mlamr_level_reduce_planned, pool.struct(), pool.state.data_ptr(),
                        ghosts.data_ptr(), child, part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, gb, gp,
                        self.sh)
+            # K6: every state value of every patch, ghost frames included (finite check)
+            self._kt1(f"k_level_reduce L{level}", e0, 8 * 3 * self.M * pool.FS)
             s = self.spec(level)
             self._call(self.lib.mlamr_sum_partials, part.data_ptr(), pool.P * bpp, self.M, s.dx * s.dy,
                        tot.data_ptr(), None, int(init), self.sh)
@@ -371,9 +423,19 @@ class Simulation:
             pl, nl = pool.work_list()
         else:
             pl, nl = bc_d.data_ptr(), n_bc
+        timed = not siblings and level > 1 and n_cells
+        e0 = self._kt0() if timed else None
         self._call(self.lib.mlamr_fill_ghosts_planned, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
                    self.prm, self.status.data_ptr(), gbase.data_ptr(), plan.data_ptr(), pl, nl, max_ghost,
                    cells.data_ptr(), n_cells, pool.interp_count.data_ptr(), bc_d.data_ptr(), n_bc, self.sh)
+        if e0 is not None:
+            # K2 on a fused level: the parent-interpolated ghost cells (the
+            # sibling copies run inside the step); per cell 3M written, the
+            # bathymetry read, 2 x 3M parent values (old, new) amortised over
+            # the r_x r_y children of a parent cell
+            M = self.M
+            self._kt1(f"k_fill_interp L{level}", e0,
+                      lambda c=pool.interp_count, f=8 * (3 * M + 1 + 2 * 3 * M / (rx * ry)): int(f * int(c.item())))
         pool.ghosts_in_cur = True
 
     # -- regridding (driver.py:192-222, regrid.py:235-353) -------------------------
@@ -582,8 +644,13 @@ class Simulation:
                 fs = self.spec(level + 1)
                 ol = old.struct() if old is not None else empty_level_struct(fs, M)
                 pl, nl = new.work_list()
+                e0 = self._kt0()
                 self._call(self.lib.mlamr_regrid_fill, new.struct(), ol, par.struct(), rx, ry, self.prm,
                            part.data_ptr(), bpp, self.status.data_ptr(), pl, nl, self.sh)
+                if e0 is not None:
+                    ob = old.boxes if old is not None else np.zeros((0, 4), np.int64)
+                    self._kt1(f"k_regrid_fill L{level + 1}", e0,
+                              lambda nb=nboxes, ob=ob: regrid_fill_bytes(nb, ob, rx, ry, M))
                 if not init:
                     self._add_delta(0, part, new.P * bpp)
             new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
@@ -669,8 +736,11 @@ class Simulation:
             raise TimeSyncError(f"level {level + 1} at t={fine.time!r} vs level {level} at t={coarse.time!r}")
         s = self.spec(level)
         cbase, n_coarse = fine.coarse_base(s.r_x, s.r_y)
+        e0 = self._kt0()
         self._call(self.lib.mlamr_average_down_flat, fine.struct(), coarse.struct(), s.r_x, s.r_y, self.prm,
                    cbase.data_ptr(), n_coarse, self.status.data_ptr(), self.sh)
+        # K4: per covered coarse cell 3M fine blocks read, 3M coarse written
+        self._kt1(f"k_average_down L{level + 1}->L{level}", e0, 8 * 3 * self.M * (s.r_x * s.r_y + 1) * n_coarse)
 
     def advance_level(self, level: int, dt: float, t0: float) -> None:
         if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:

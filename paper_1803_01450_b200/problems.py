@@ -476,4 +476,21 @@ def config3(seed: int = 3, n_coarse_steps: int = 100, nx0: int = 256) -> Problem
     return pb
 
 
-CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}
+def config5_stress(seed: int = 5, n_coarse_steps: int = 100, nx0: int = 1280, p: float = 0.05) -> Problem:
+    """C5 as a regrid stress that actually regrids: with Bernoulli(0.3)
+    flags dilated by one cell nearly every level-1 cell is flagged, the
+    clustered layout is the same every step and C5 performs no rebuild at
+    all (profiles/r01/README.md); at p = 0.05 the dilated flags cover ~37 %
+    of level 1 and the level-2 layout (~75 k 16x16 patches) is rebuilt --
+    refine, copy, derefine -- in every coarse step.  Its dynamic-r_t rule
+    (pick_rt, from the speeds before the rebuild) meets the reference's CFL
+    guard in the fourth coarse step (t = 19.17): freshly refined patches are
+    faster than the ones r_t was chosen for."""
+    pb = config5(seed, n_coarse_steps, nx0)
+    pb.name = "C5s"
+    pb.bernoulli = (p,)
+    pb.flag_rule = ("bernoulli", p, 1)
+    return pb
+
+
+CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5, "C5s": config5_stress}

@@ -42,13 +42,7 @@ def problem(name: str):
     every coarse step, unlike p = 0.3 whose dilated flags cover ~96 % of
     the level and cluster to the same chopped layout every step)."""
     from paper_1803_01450_b200 import problems
-    if name == "C5s":
-        pb = problems.config5()
-        pb.bernoulli = (0.05,)
-        pb.flag_rule = ("bernoulli", 0.05, 1)
-        pb.name = "C5s"
-        return pb
-    return problems.CONFIGS[name]()
+    return problems.CONFIGS[name]()   # C5s: problems.config5_stress
 
 
 def ref_variant(name: str):
