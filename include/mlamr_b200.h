@@ -341,6 +341,18 @@ int mlamr_flags_gradient(mlamr_level lv, const double *state, mlamr_params prm, 
                          double tol, int dilate_w, uint8_t *flags, uint8_t *allowed, uint8_t *scratch,
                          double *eta_scratch, void *stream);
 
+/* The gradient rule for a sharded level, in two halves around the union
+ * (uint8 MAX all-reduce) of the ranks' raw flags: _raw evaluates the rule
+ * on the rank's local pool and keeps the owned cells' flags
+ * (owned_patches: uint8 per local patch, NULL = all); _finish dilates the
+ * union and masks it with the level's GLOBAL coverage (0/1 map) and its
+ * one-cell erosion (allowed).  bits: ny*nx bytes; scratch: 3*ny*nx. */
+int mlamr_flags_gradient_raw(mlamr_level lv, const double *state, mlamr_params prm, unsigned layer_mask,
+                             double tol, const uint8_t *owned_patches, uint8_t *raw, uint8_t *bits,
+                             double *eta_scratch, void *stream);
+int mlamr_flags_finish(const uint8_t *raw, const uint8_t *covered, int ny, int nx, int dilate_w,
+                       uint8_t *flags, uint8_t *allowed, uint8_t *scratch, void *stream);
+
 /* Summed-area table for the clustering bisection (regrid.cluster_flags,
  * regrid.py:129-182): sat is int32 [(ny+1)*(nx+1)] with
  * sat[(j+1)*(nx+1)+(i+1)] = sum over [0,j]x[0,i] of map (invert=0) or

@@ -115,6 +115,10 @@ SIGNATURES = {
     "mlamr_flags_bernoulli": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong,
                                              ctypes.c_ulonglong, ctypes.c_double, ctypes.c_int, c_vp, c_vp, c_vp,
                                              c_vp]),
+    "mlamr_flags_gradient_raw": (ctypes.c_int, [Level, c_vp, Params, ctypes.c_uint, ctypes.c_double, c_vp, c_vp,
+                                                c_vp, c_vp, c_vp]),
+    "mlamr_flags_finish": (ctypes.c_int, [c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp, c_vp, c_vp,
+                                          c_vp]),
     "mlamr_flags_gradient": (ctypes.c_int, [Level, c_vp, Params, ctypes.c_uint, ctypes.c_double, ctypes.c_int,
                                             c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_copy_pairs_of_plan": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, c_vp, ctypes.c_int, c_vp,

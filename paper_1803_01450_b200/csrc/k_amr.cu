@@ -1669,6 +1669,12 @@ __global__ void k_grad_eta(mlamr_level lv, const double *__restrict__ state, uns
     }
 }
 
+__global__ void k_cov_bits(const uint8_t *covered, uint8_t *bits, int64_t n) {
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x)
+        bits[idx] = covered[idx] ? 0x80 : 0;
+}
+
 __global__ void k_grad_flags(const double *__restrict__ eta, int K, const uint8_t *__restrict__ bits, int ny,
                              int nx, double dx, double dy, double tol, uint8_t *__restrict__ flag) {
     const int64_t n = (int64_t)ny * nx;
@@ -1719,6 +1725,64 @@ extern "C" int mlamr_flags_gradient(mlamr_level lv, const double *state, mlamr_p
     k_morph3<<<nb, 256, 0, st>>>(b, allowed, ny, nx, 1);
     k_flag_mask<<<nb, 256, 0, st>>>(a, bits, allowed, n);
     cudaMemcpyAsync(flags, a, n, cudaMemcpyDeviceToDevice, st);
+    return (int)cudaGetLastError();
+}
+
+// Sharded form of the gradient rule, in two halves around the all-reduce of
+// the raw flags.  The raw half evaluates the rule on a rank's local pool
+// (owned patches + shadows: every covered neighbour of an owned cell lies
+// in a held sibling's refreshed interior ring) and keeps the flags of owned
+// cells only; the finish half dilates the union and masks it with the
+// GLOBAL coverage (0/1 map of the level's whole layout) and its erosion.
+__global__ void k_flags_owned_only(const int32_t *own, int ny, int nx, const uint8_t *owned, uint8_t *flag) {
+    const int64_t n = (int64_t)ny * nx;
+    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int j = (int)(idx / nx), i = (int)(idx - (int64_t)j * nx);
+        const int o = owner_at(own, nx, ny, i, j);
+        if (o < 0 || !owned[o]) flag[idx] = 0;
+    }
+}
+
+extern "C" int mlamr_flags_gradient_raw(mlamr_level lv, const double *state, mlamr_params prm, unsigned layer_mask,
+                                        double tol, const uint8_t *owned_patches, uint8_t *raw, uint8_t *bits,
+                                        double *eta_scratch, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    const int ny = lv.level_ny, nx = lv.level_nx;
+    const int64_t n = (int64_t)ny * nx;
+    if (n <= 0) return 0;
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
+        constexpr int M = decltype(Mc)::value;
+        k_grad_eta<M><<<nb, 256, 0, st>>>(lv, state, layer_mask, eta_scratch, bits);
+    });
+    if (rc) return rc;
+    const int K = __builtin_popcount(layer_mask & ((1u << prm.num_layers) - 1u));
+    k_grad_flags<<<nb, 256, 0, st>>>(eta_scratch, K, bits, ny, nx, lv.dx, lv.dy, tol, raw);
+    if (owned_patches != nullptr) k_flags_owned_only<<<nb, 256, 0, st>>>(lv.own, ny, nx, owned_patches, raw);
+    return (int)cudaGetLastError();
+}
+
+extern "C" int mlamr_flags_finish(const uint8_t *raw, const uint8_t *covered, int ny, int nx, int dilate_w,
+                                  uint8_t *flags, uint8_t *allowed, uint8_t *scratch, void *stream) {
+    cudaStream_t st = as_stream(stream);
+    const int64_t n = (int64_t)ny * nx;
+    if (n <= 0) return 0;
+    const int nb = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+    uint8_t *a = scratch, *b = scratch + n, *bits = scratch + 2 * n;
+    cudaError_t e = cudaMemcpyAsync(a, raw, n, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return (int)e;
+    for (int w = 0; w < dilate_w; ++w) {
+        k_morph3<<<nb, 256, 0, st>>>(a, b, ny, nx, 0);
+        uint8_t *t = a; a = b; b = t;
+    }
+    // coverage bits in the 0x80 convention of k_covered / k_flag_mask
+    k_cov_bits<<<nb, 256, 0, st>>>(covered, bits, n);
+    k_covered<<<nb, 256, 0, st>>>(bits, b, n);
+    k_morph3<<<nb, 256, 0, st>>>(b, allowed, ny, nx, 1);
+    k_flag_mask<<<nb, 256, 0, st>>>(a, bits, allowed, n);
+    e = cudaMemcpyAsync(flags, a, n, cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) return (int)e;
     return (int)cudaGetLastError();
 }
 

@@ -441,17 +441,20 @@ class LevelPool:
         """Local indices of global patch indices (all must be held)."""
         return np.searchsorted(self.gidx, g)
 
-    def copy_segments(self, src_buf, src_stride, dst_buf, dst_stride, src_off, dst_off, sizes) -> None:
-        """Whole-block copies of all 3M planes (multi-GPU shadow exchange)."""
+    def copy_segments(self, src_buf, src_stride, dst_buf, dst_stride, src_off, dst_off, sizes,
+                      stream: Optional[torch.cuda.Stream] = None) -> None:
+        """Whole-block copies of all 3M planes (multi-GPU shadow exchange),
+        on ``stream`` (default: the pool's)."""
         n = len(sizes)
         if n == 0:
             return
+        st = stream or self.stream
         seg = np.stack([np.asarray(src_off, np.int64), np.asarray(dst_off, np.int64),
                         np.asarray(sizes, np.int64)], axis=1)
-        seg_d = arena().upload(seg, self.device, self.stream)
+        seg_d = arena().upload(seg, self.device, st)
         N.check(N.lib().mlamr_copy_segments(src_buf.data_ptr(), int(src_stride), dst_buf.data_ptr(),
                                             int(dst_stride), seg_d.data_ptr(), n, int(np.max(sizes)),
-                                            3 * self.M, self.stream.cuda_stream), "copy_segments")
+                                            3 * self.M, st.cuda_stream), "copy_segments")
 
     def blocks_per_patch(self, cells: int) -> int:
         return int(max(1, min(64, (cells + NTHREADS - 1) // NTHREADS)))

@@ -33,7 +33,7 @@ import torch.distributed as dist
 
 from . import _native as N
 from .device import LevelPool, empty_level_struct, paint_child_map
-from .distributed import (Comm, _any_meet, needed, partition, patch_sizes, plan_acquire, plan_refresh,
+from .distributed import (Comm, Transfer, _any_meet, needed, partition, patch_sizes, plan_acquire, plan_refresh,
                           ring_segments, run_transfer)
 from .driver import Simulation
 from .mesh import GHOST_WIDTH, IndexBox, boxes_array
@@ -47,8 +47,7 @@ class ShardedSimulation(Simulation):
                  reserve_factor: float = 1.0, _restore: dict | None = None):
         self._init_sharding(comm)
         self._common_init(problem, device, stream)
-        if self.pb.flag_rule[0] == "gradient":
-            raise NotImplementedError("sharded runs support the reference and Bernoulli flag rules")
+        self._xstream = torch.cuda.Stream(device=self.dev)
         if _restore is not None:
             self._restore_from(_restore)
             return
@@ -76,6 +75,7 @@ class ShardedSimulation(Simulation):
         # children); the other shadows are refreshed as interior rings
         self.full = {}
         self.ring_refresh = True
+        self._xstream = None   # the shadow-exchange stream (set with the device)
         self._ring_cache = {}
         self._fullc_cache = {}
         self.bytes_exchanged = 0
@@ -173,7 +173,8 @@ class ShardedSimulation(Simulation):
             self._ring_cache[level] = ent
         return ent[1:]
 
-    def _transfer(self, level, tr, src: LevelPool, dst: LevelPool) -> None:
+    def _transfer(self, level, tr, src: LevelPool, dst: LevelPool, stream=None) -> None:
+        st = stream or self.stream
         full_sz = patch_sizes(self.layout[level])
         ro, ln, rsize, cnt, start = self._ring_table(level)
         M3 = 3 * self.M
@@ -207,29 +208,36 @@ class ShardedSimulation(Simulation):
         def pack(g, ring, src_off, buf):
             a, pk, lens = runs(g, ring, src_off)
             n = int(nsz(g, ring).sum())
-            src.copy_segments(src.state, src.FS, buf, n, a, pk, lens)
+            src.copy_segments(src.state, src.FS, buf, n, a, pk, lens, stream=st)
 
         def unpack(g, ring, buf, dst_off):
             a, pk, lens = runs(g, ring, dst_off)
             n = int(nsz(g, ring).sum())
-            dst.copy_segments(buf, n, dst.state, dst.FS, pk, a, lens)
+            dst.copy_segments(buf, n, dst.state, dst.FS, pk, a, lens, stream=st)
 
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(st):
             self.bytes_exchanged += run_transfer(
                 self.comm, tr, nsz, M3, lambda g: src.offsets[src.local_of(g)],
                 lambda g: dst.offsets[dst.local_of(g)], pack, unpack, torch.float64, self.dev)
 
-    def _refresh(self, level: int, coarsen: bool = False) -> None:
+    def _refresh(self, level: int, coarsen: bool = False, full_only: bool = False, stream=None) -> None:
         """Shadow refresh; ``coarsen``: the one in front of averaging this
-        level down, which must deliver children whole."""
+        level down, which must deliver children whole.  ``full_only``: only
+        the shadows held in full (their frames were just filled; the
+        ring-only ones have not changed since the last refresh)."""
         if self.world == 1 or level not in self.levels:
             return
         full = None
         if self.ring_refresh:
             full = self._full_coarsen(level) if coarsen else self.full.get(level)
         tr = plan_refresh(self.rank, self.world, self.held[level], self.owner[level], full)
+        if full_only and tr.send_ring is not None:
+            keep = lambda d, ring: {q: g[~ring[q]] for q, g in d.items() if (~ring[q]).any()}
+            tr = Transfer(keep(tr.send, tr.send_ring), keep(tr.recv, tr.recv_ring),
+                          {q: np.zeros(int((~r).sum()), bool) for q, r in tr.send_ring.items() if (~r).any()},
+                          {q: np.zeros(int((~r).sum()), bool) for q, r in tr.recv_ring.items() if (~r).any()})
         pool = self.levels[level]
-        self._transfer(level, tr, pool, pool)
+        self._transfer(level, tr, pool, pool, stream=stream)
 
     def _reshape(self, level: int, new_held, new_full=None) -> None:
         """Replace a level's local pool by one holding new_held[rank] (same
@@ -354,14 +362,48 @@ class ShardedSimulation(Simulation):
     def _reduce_flag_bits(self, bits) -> None:
         """Each rank wrote the bits of its owned cells only: max == union."""
         if self.world > 1:
-            wide = bits.to(torch.int32)
-            self.comm.allreduce(wide, dist.ReduceOp.MAX)
-            bits.copy_(wide.to(torch.uint8))
+            self.comm.allreduce(bits, dist.ReduceOp.MAX)   # uint8 in place
 
     def _device_rule(self) -> bool:
         # a rank's owner maps hold only its local patches: Bernoulli coverage
-        # comes from the global layout on the host
-        return self.pb.flag_rule[0] == "reference"
+        # comes from the global layout on the host; the gradient rule runs
+        # in two device halves around the union of the owned flags
+        return self.pb.flag_rule[0] in ("reference", "gradient")
+
+    def _device_flags(self, level: int):
+        if self.pb.flag_rule[0] != "gradient":
+            return super()._device_flags(level)
+        from .device import arena
+        from .mesh import paint
+        pool = self.levels[level]
+        s = self.spec(level)
+        b = self._flag_buffers(level)
+        _, tol, width, layers = self.pb.flag_rule
+        mask = 0
+        for m in layers:
+            mask |= 1 << int(m)
+        key = ("eta", level)
+        with torch.cuda.stream(self.stream):
+            if key not in self._flagbuf:
+                self._flagbuf[key] = torch.empty(len(layers) * s.ny * s.nx, dtype=torch.float64, device=self.dev)
+            n = s.ny * s.nx
+            if pool.P:
+                owned = arena().upload(np.asarray(pool.owned, np.uint8), self.dev, self.stream)
+                self._call(self.lib.mlamr_flags_gradient_raw, pool.struct(), pool.state.data_ptr(), self.prm, mask,
+                           float(tol), owned.data_ptr(), b["bits"].data_ptr(), b["scratch"].data_ptr(),
+                           self._flagbuf[key].data_ptr(), self.sh)
+            else:
+                b["bits"].zero_()
+            self._reduce_flag_bits(b["bits"])          # union of the ranks' owned flags
+            cov = arena().upload(paint(self.layout[level], s.ny, s.nx).astype(np.uint8).reshape(-1),
+                                 self.dev, self.stream)
+            self._call(self.lib.mlamr_flags_finish, b["bits"].data_ptr(), cov.data_ptr(), s.ny, s.nx, int(width),
+                       b["flags"].data_ptr(), b["allowed"].data_ptr(), b["scratch"].data_ptr(), self.sh)
+            region = self._region_mask_d(level)
+            if region is not None:
+                b["flags"].mul_(region)
+                b["allowed"].mul_(region)
+        return b["flags"], b["allowed"]
 
     def flags_and_allowed(self, level: int):
         s = self.spec(level)
@@ -479,13 +521,25 @@ class ShardedSimulation(Simulation):
         fuse = self.fuse_sibling_fill and not has_child
         self.fill_level_ghosts(level, t0, siblings=not fuse)
         self.levels[level].fused_frame = fuse   # the finite check reads its sibling cells via the plan
-        self._refresh(level)                                            # (ii)
+        ev = None
+        if has_child:
+            # (ii) the full shadows (parents of the children), frames just
+            # filled at t0, on the exchange stream: the step reads owned
+            # frames and sibling interiors only, so the exchange overlaps
+            # it; the children's fills (stash = this buffer) wait for it.
+            # A childless level skips (ii): its shadows are ring-only and
+            # unchanged since (i).
+            self._xstream.wait_stream(self.stream)
+            self._refresh(level, full_only=True, stream=self._xstream)      # (ii)
+            ev = torch.cuda.Event()
+            ev.record(self._xstream)
         pool = self.levels[level]
         self._step_patches(level, dt, fused_siblings=fuse)
         self.steps[level] += 1
         t1 = t0 + dt
         pool.time = t1
         if has_child:
+            self.stream.wait_event(ev)
             self.fill_level_ghosts(level, t1)
             self._refresh(level)                                        # (iii)
             self._stash[level] = (t0, dt, pool.other)

@@ -29,6 +29,10 @@ def variant(name):
         pb = problems.config4(nx0=64)
         pb.regrid_interval = 2
         return pb, 2
+    if name == "C3":
+        pb = problems.config3(nx0=32)   # M = 3, gradient flag rule, dynamic r_t
+        pb.regrid_interval = 2
+        return pb, 3
     if name == "C5":
         pb = problems.config5(nx0=64)
         pb.bernoulli = (0.05,)

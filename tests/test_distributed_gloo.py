@@ -1,5 +1,5 @@
 """Multi-rank host logic of the sharded path (distributed.py) with the gloo
-backend on CPU, world size 2: SFC partition, shadow rules, transfer plans
+backend on CPU, world sizes 2 and 4: SFC partition, shadow rules, transfer plans
 and the whole-patch exchange (with host tensors standing in for device
 pools; the CUDA pack kernel is exercised by tests/test_gpu_sharded.py)."""
 
@@ -120,13 +120,20 @@ def _worker(rank, world, port, q):
         sent = {q: g.tolist() for q, g in tr.send.items()}
         recv = {q: g.tolist() for q, g in tr.recv.items()}
         t = torch.tensor([comm.allreduce(torch.ones(1)).item()])
+        # flag bits: a uint8 MAX all-reduce in place is the union of the
+        # ranks' owned bits (sharded._reduce_flag_bits)
+        bits = torch.zeros(64, dtype=torch.uint8)
+        bits[rank::world] = 1 << (rank % 8)
+        comm.allreduce(bits, dist.ReduceOp.MAX)
+        want = torch.tensor([1 << (k % world % 8) for k in range(64)], dtype=torch.uint8)
+        assert torch.equal(bits, want), bits
         q.put((rank, results, sent, recv, t.item()))
     finally:
         dist.destroy_process_group()
 
 
-def test_sharded_exchange_world2():
-    world = 2
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_exchange(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()

@@ -21,7 +21,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name", ["C2", "C4", "C5"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
 def test_sharded_two_ranks_match_single_gpu(name):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
