@@ -386,8 +386,11 @@ __global__ void __launch_bounds__(NTA) k_copy_pairs_of_plan(mlamr_level lv, cons
 }
 
 // coarse interpolation of the cells of a compacted list (patch, ghost idx)
+#ifndef MLAMR_INTERP_MINB
+#define MLAMR_INTERP_MINB 1
+#endif
 template <int M>
-__global__ void __launch_bounds__(NTA) k_fill_interp(mlamr_level lv, mlamr_level par, const double *par_old,
+__global__ void __launch_bounds__(NTA, MLAMR_INTERP_MINB) k_fill_interp(mlamr_level lv, mlamr_level par, const double *par_old,
                                                      double theta, int r_x, int r_y, const int32_t *cells,
                                                      int n_cells, const int32_t *n_cells_dev, mlamr_params prm,
                                                      const int32_t *status) {

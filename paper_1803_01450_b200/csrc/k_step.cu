@@ -38,6 +38,25 @@ struct StepConst {
     double coef;          // g * (1 - rho_0 / rho_1), the shear bound (physics.py:306)
 };
 
+// ceil(2^16 / w) for the step's compact rectangle iteration (step_tile.cuh):
+// q = (idx * c_div_magic[w]) >> 16 == idx / w for every idx < 65536 / w.
+__constant__ unsigned c_div_magic[64] = {
+    0u,
+#define MLAMR_MAGIC(w) (65536u + (w) - 1u) / (w)
+    MLAMR_MAGIC(1), MLAMR_MAGIC(2), MLAMR_MAGIC(3), MLAMR_MAGIC(4), MLAMR_MAGIC(5), MLAMR_MAGIC(6),
+    MLAMR_MAGIC(7), MLAMR_MAGIC(8), MLAMR_MAGIC(9), MLAMR_MAGIC(10), MLAMR_MAGIC(11), MLAMR_MAGIC(12),
+    MLAMR_MAGIC(13), MLAMR_MAGIC(14), MLAMR_MAGIC(15), MLAMR_MAGIC(16), MLAMR_MAGIC(17), MLAMR_MAGIC(18),
+    MLAMR_MAGIC(19), MLAMR_MAGIC(20), MLAMR_MAGIC(21), MLAMR_MAGIC(22), MLAMR_MAGIC(23), MLAMR_MAGIC(24),
+    MLAMR_MAGIC(25), MLAMR_MAGIC(26), MLAMR_MAGIC(27), MLAMR_MAGIC(28), MLAMR_MAGIC(29), MLAMR_MAGIC(30),
+    MLAMR_MAGIC(31), MLAMR_MAGIC(32), MLAMR_MAGIC(33), MLAMR_MAGIC(34), MLAMR_MAGIC(35), MLAMR_MAGIC(36),
+    MLAMR_MAGIC(37), MLAMR_MAGIC(38), MLAMR_MAGIC(39), MLAMR_MAGIC(40), MLAMR_MAGIC(41), MLAMR_MAGIC(42),
+    MLAMR_MAGIC(43), MLAMR_MAGIC(44), MLAMR_MAGIC(45), MLAMR_MAGIC(46), MLAMR_MAGIC(47), MLAMR_MAGIC(48),
+    MLAMR_MAGIC(49), MLAMR_MAGIC(50), MLAMR_MAGIC(51), MLAMR_MAGIC(52), MLAMR_MAGIC(53), MLAMR_MAGIC(54),
+    MLAMR_MAGIC(55), MLAMR_MAGIC(56), MLAMR_MAGIC(57), MLAMR_MAGIC(58), MLAMR_MAGIC(59), MLAMR_MAGIC(60),
+    MLAMR_MAGIC(61), MLAMR_MAGIC(62), MLAMR_MAGIC(63)
+#undef MLAMR_MAGIC
+};
+
 // K1 in two tile shapes: 16x32 interior tiles (320 threads, 2 CTAs/SM) for
 // levels whose patches are wider than 16 cells, 16x16 tiles (192 threads,
 // 4 CTAs/SM) for narrow-patch levels (C5's 16x16 patches would leave half

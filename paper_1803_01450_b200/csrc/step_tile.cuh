@@ -31,18 +31,25 @@ struct StepSmem {
 };
 
 // All shared-memory phases iterate a rectangle [r0,r1) x [c0,c1) of the
-// padded tile in row-major order with the compile-time row pitch PX, so the
-// index split is a multiply-shift (runtime integer division costs three XU
-// ops and saturated the XU pipe in the first profile) and consecutive
-// threads touch consecutive doubles (no bank conflicts in either sweep
-// direction).
+// padded tile in row-major order over the rectangle itself (compact: a
+// ragged tile -- 16.5 % of C4's level-3 tile slots are outside patches --
+// costs iterations in proportion to its cells, not to the full tile), with
+// consecutive threads on consecutive cells of a row (no bank conflicts in
+// either sweep direction).  The row split divides by the runtime width w
+// with a reciprocal table, q = (idx * ceil(2^16/w)) >> 16, which is
+// floor(idx/w) whenever idx/65536 < 1/w (the rounding-up error stays below
+// the gap to the next integer) -- every rectangle here (idx < 612, w <= 34):
+// one multiply and a shift, the cost of the compile-time pitch it replaces
+// (runtime integer division costs three XU ops and saturated the XU pipe in
+// the first profile).  Storage keeps the compile-time pitch PX.
 // (a begin/end macro pair rather than a macro taking the body, so the
 // body keeps its own source lines in the profiler's source view)
-#define FOR_RECT_BEGIN(r0, r1, c0, c1)                                   \
-    for (int idx_ = threadIdx.x; idx_ < ((r1) - (r0)) * PX; idx_ += NT) { \
-        const int r = (r0) + idx_ / PX;                                  \
-        const int c = idx_ - (idx_ / PX) * PX;                           \
-        if (c < (c0) || c >= (c1)) continue;
+#define FOR_RECT_BEGIN(r0, r1, c0, c1)                                        \
+    for (int w_ = (c1) - (c0), m_ = (int)c_div_magic[w_], idx_ = threadIdx.x; \
+         idx_ < ((r1) - (r0)) * w_; idx_ += NT) {                             \
+        const int q_ = (int)(((unsigned)idx_ * (unsigned)m_) >> 16);          \
+        const int r = (r0) + q_;                                              \
+        const int c = (c0) + idx_ - q_ * w_;
 #define FOR_RECT_END }
 
 
@@ -395,12 +402,14 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
     for (int it = 0; it < (NEXT ? MAXIT : 1); ++it) k2s[it] = -1;
     const unsigned char *CWc = cowet_pl<M, SW>(s);
 #pragma unroll
+    const int uw = uc1 - uc0;
+    const unsigned um = c_div_magic[uw];
     for (int it = 0; it < MAXIT; ++it) {
         const int idx_ = threadIdx.x + it * NT;
-        if (idx_ >= (ur1 - ur0) * PX) break;
-        const int r = ur0 + idx_ / PX;
-        const int c = idx_ - (idx_ / PX) * PX;
-        if (c < uc0 || c >= uc1) continue;
+        if (idx_ >= (ur1 - ur0) * uw) break;
+        const int q_ = (int)(((unsigned)idx_ * um) >> 16);
+        const int r = ur0 + q_;
+        const int c = uc0 + idx_ - q_ * uw;
         const int k = r * PX + c;
         const int km = k - STEP, kp = k + STEP;
         const bool copl = AW || (CWc[km] && CWc[k]);
@@ -562,12 +571,15 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
         const double *ga[NITEM];
         bool in[NITEM], fr[NITEM];
         int64_t gv[NITEM];
+        const unsigned sm_ = c_div_magic[nx2];
 #pragma unroll
         for (int i = 0; i < NITEM; ++i) {
+            // the compact mapping of FOR_RECT over the padded tile: the
+            // first sweep's phase A reads exactly the cells its thread staged
             const int idx = t + i * NT;
-            const int r = idx / PX, c = idx - (idx / PX) * PX;
-            in[i] = idx < ny2 * PX && c < nx2;
-            sa[i] = (unsigned)__cvta_generic_to_shared(&s.S[0][0]) + idx * 8;
+            const int r = (int)(((unsigned)idx * sm_) >> 16), c = idx - r * nx2;
+            in[i] = idx < ny2 * nx2;
+            sa[i] = (unsigned)__cvta_generic_to_shared(&s.S[0][0]) + (r * PX + c) * 8;
             ga[i] = src + base + (int64_t)r * pv.NX + c;
             fr[i] = false;
             gv[i] = -1;

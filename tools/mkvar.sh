@@ -7,6 +7,6 @@ for v in "$@"; do
   set -- $v; name=$1; shift
   ( nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo -fmad=false -Xcompiler -fPIC,-fopenmp -lgomp \
       -shared -I../include "$@" -Xptxas -v -o _lib/var/$name.so csrc/k_step.cu csrc/k_amr.cu csrc/patch_table.cu csrc/host_cluster.cpp 2>&1 \
-      | grep -A3 "walk6k_stepILi2ELb0" | grep -E "registers|spill" | tr '\n' ' ' | sed 's/ptxas info    ://g'; echo " <- $name $*" ) &
+      | grep -A3 "${GREPK:-walk6k_stepILi2ELb0}" | grep -E "registers|spill" | tr '\n' ' ' | sed 's/ptxas info    ://g'; echo " <- $name $*" ) &
 done
 wait
