@@ -311,7 +311,7 @@ def b200_arm(args):
     peak, peak_kind = _peaks()
     traffic, traffic_ratio = None, None
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "step_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02", "step_traffic.json")) as f:
             tj = json.load(f)
         traffic, traffic_ratio = tj["dram_bytes"], tj["traffic_over_algorithmic"]
     except Exception:
@@ -406,7 +406,7 @@ def b200_arm(args):
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "traffic_over_algorithmic": traffic_ratio,
                          "traffic_source": "ncu --set full capture of one C4 level-3 launch "
-                                           "(profiles/r01/step_traffic.json)",
+                                           "(profiles/r02/step_traffic.json)",
                          "kernel": "mlamr_step (k_step) on the finest level",
                          "bytes_per_launch": int(np.mean(byts)) if byts else None,
                          "avg_launch_ms": 1e3 * float(np.mean(durs)) if durs else None,
