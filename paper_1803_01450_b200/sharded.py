@@ -76,6 +76,13 @@ class ShardedSimulation(Simulation):
         self.full = {}
         self.ring_refresh = True
         self._xstream = None   # the shadow-exchange stream (set with the device)
+        # (ii) on the exchange stream, overlapping the step.  Off by default:
+        # with NCCL it puts point-to-point traffic on a second stream next to
+        # the driver stream's collectives, which this build could not run
+        # (one GPU; NCCL refuses two ranks on one device).  The gloo tests
+        # exercise it (tests/test_gpu_sharded.py sets MLAMR_OVERLAP_REFRESH).
+        import os as _os
+        self.overlap_refresh = _os.environ.get("MLAMR_OVERLAP_REFRESH", "0") == "1"
         self._ring_cache = {}
         self._fullc_cache = {}
         self.bytes_exchanged = 0
@@ -524,22 +531,26 @@ class ShardedSimulation(Simulation):
         ev = None
         if has_child:
             # (ii) the full shadows (parents of the children), frames just
-            # filled at t0, on the exchange stream: the step reads owned
-            # frames and sibling interiors only, so the exchange overlaps
-            # it; the children's fills (stash = this buffer) wait for it.
-            # A childless level skips (ii): its shadows are ring-only and
-            # unchanged since (i).
-            self._xstream.wait_stream(self.stream)
-            self._refresh(level, full_only=True, stream=self._xstream)      # (ii)
-            ev = torch.cuda.Event()
-            ev.record(self._xstream)
+            # filled at t0.  A childless level skips (ii): its shadows are
+            # ring-only and unchanged since (i).  With overlap_refresh the
+            # exchange runs on its own stream while the step runs (the step
+            # reads owned frames and sibling interiors only); the t1 fill
+            # and the children's fills (stash = this buffer) wait for it.
+            if self.overlap_refresh:
+                self._xstream.wait_stream(self.stream)
+                self._refresh(level, full_only=True, stream=self._xstream)  # (ii)
+                ev = torch.cuda.Event()
+                ev.record(self._xstream)
+            else:
+                self._refresh(level, full_only=True)                       # (ii)
         pool = self.levels[level]
         self._step_patches(level, dt, fused_siblings=fuse)
         self.steps[level] += 1
         t1 = t0 + dt
         pool.time = t1
         if has_child:
-            self.stream.wait_event(ev)
+            if ev is not None:
+                self.stream.wait_event(ev)
             self.fill_level_ghosts(level, t1)
             self._refresh(level)                                        # (iii)
             self._stash[level] = (t0, dt, pool.other)

@@ -21,11 +21,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4", "C5"])
-def test_sharded_two_ranks_match_single_gpu(name):
+@pytest.mark.parametrize("name,overlap", [("C2", "0"), ("C2", "1"), ("C3", "0"), ("C4", "1"), ("C5", "0")])
+def test_sharded_two_ranks_match_single_gpu(name, overlap):
+    """overlap = MLAMR_OVERLAP_REFRESH: the parents' refresh (ii) on its own
+    stream, overlapping the step."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(HERE, "dist_gpu_worker.py"), name]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=420)
+    env = dict(os.environ, MLAMR_OVERLAP_REFRESH=overlap)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("sharded == single-GPU") == 2, r.stdout[-2000:]
