@@ -185,6 +185,20 @@ class Comm:
             dist.all_reduce(t, op=op)
         return t
 
+    def warmup_p2p(self, device) -> None:
+        """One ring exchange in which every rank takes part.  With NCCL the
+        first batch_isend_irecv of a group must involve all its ranks, and
+        later exchanges skip ranks with nothing to move."""
+        if self.world == 1:
+            return
+        dev = torch.device("cpu") if self.staged else device
+        s = torch.full((1,), float(self.rank), dtype=torch.float64, device=dev)
+        r = torch.empty(1, dtype=torch.float64, device=dev)
+        ops = [dist.P2POp(dist.isend, s, (self.rank + 1) % self.world),
+               dist.P2POp(dist.irecv, r, (self.rank - 1) % self.world)]
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+
     def exchange(self, sends: Dict[int, torch.Tensor], recvs: Dict[int, torch.Tensor]) -> None:
         """Grouped point-to-point transfer: sends[peer] -> peer, recvs[peer] <- peer."""
         if self.world == 1 or (not sends and not recvs):

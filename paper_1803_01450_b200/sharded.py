@@ -48,6 +48,8 @@ class ShardedSimulation(Simulation):
         self._init_sharding(comm)
         self._common_init(problem, device, stream)
         self._xstream = torch.cuda.Stream(device=self.dev)
+        with torch.cuda.stream(self.stream):
+            self.comm.warmup_p2p(self.dev)
         if _restore is not None:
             self._restore_from(_restore)
             return

@@ -48,6 +48,7 @@ def _worker(rank, world, port, q):
                                                        plan_refresh, ring_segments, run_transfer)
         comm = Comm()
         assert comm.world == world and comm.rank == rank
+        comm.warmup_p2p(torch.device("cpu"))   # every rank in the first batch_isend_irecv
         layouts = _layouts()
         ratios = {1: (4, 4), 2: (4, 4), 3: (1, 1)}
         owners = {1: np.zeros(1, np.int32), 2: partition(layouts[2], 4, 4, world),
