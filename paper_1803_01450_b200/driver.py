@@ -818,10 +818,11 @@ class Simulation:
         for lev in range(1, self.L):
             s = self.spec(lev)
             fs = self.spec(lev + 1)
-            sp = self.level_speed(lev + 1)
-            vmax = 0.0
-            for v in sp:
-                vmax = max(vmax, float(v))
+            sp = np.atleast_1d(np.asarray(self.level_speed(lev + 1), dtype=np.float64))
+            # the running Python max from 0.0 skips NaN speeds (a NaN never
+            # compares greater): the maximum of the non-NaN ones, floored at 0
+            ok = sp[~np.isnan(sp)]
+            vmax = max(0.0, float(ok.max())) if ok.size else 0.0
             rt = self.pb.pick_rt(vmax, dtl, min(fs.dx, fs.dy), max(s.r_x, s.r_y))
             self.specs[lev - 1] = replace(s, r_t=rt)
             dtl = dtl / rt
