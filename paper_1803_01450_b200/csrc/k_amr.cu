@@ -684,12 +684,12 @@ __global__ void __launch_bounds__(NTA) k_check_bathy(mlamr_level fine, mlamr_lev
 // r_x*r_y children from the old patch covering them, or refine them from
 // the parent's interiors (gather include_ghosts=False, regrid.py:295-300).
 // ---------------------------------------------------------------------------
-template <int M>
-__global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
+template <int M, int NTR = NTA>
+__global__ void __launch_bounds__(NTR) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
                                                      int r_x, int r_y, mlamr_params prm,
                                                      double *refine_delta, int32_t *status, const int32_t *plist,
                                                      int nrows) {
-    __shared__ double red[NTA];
+    __shared__ double red[NTR];
     const int row = grid_row();
     if (row >= nrows) return;
     const int p = plist ? plist[row] : row;
@@ -712,8 +712,8 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
     // independent cells in flight are what reaches the bandwidth.
     constexpr int RG = 4;
     const int ncell = nv.nx * nv.ny;
-    const int stride = gridDim.x * NTA;
-    for (int base = blockIdx.x * NTA + threadIdx.x; base < ncell; base += RG * stride) {
+    const int stride = gridDim.x * NTR;
+    for (int base = blockIdx.x * NTR + threadIdx.x; base < ncell; base += RG * stride) {
         int64_t ks[RG], kd[RG];
 #pragma unroll
         for (int u = 0; u < RG; ++u) {
@@ -742,7 +742,7 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
 #pragma unroll
                 for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + kd[u]] = v[u][f];
     }
-    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
+    for (int idx = blockIdx.x * NTR + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTR) {
         const int J = idx / cnx, I = idx % cnx;
         const int ci = clo_i + I, cj = clo_j + J;
         const int fi0 = ci * r_x, fj0 = cj * r_y;
@@ -778,18 +778,18 @@ __global__ void __launch_bounds__(NTA) k_regrid_fill(mlamr_level nl, mlamr_level
     }
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-        const double s = block_sum<NTA>(dsum[m], red);
+        const double s = block_sum<NTR>(dsum[m], red);
         if (threadIdx.x == 0) refine_delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
     }
 }
 
 // derefine delta (regrid.py:329-348): coarse cells covered by an old patch
 // but by no new one: coarse mass minus the discarded fine mass.
-template <int M>
-__global__ void __launch_bounds__(NTA) k_derefine(mlamr_level ol, mlamr_level par, const int32_t *new_child,
+template <int M, int NTR = NTA>
+__global__ void __launch_bounds__(NTR) k_derefine(mlamr_level ol, mlamr_level par, const int32_t *new_child,
                                                   int r_x, int r_y, double *delta, const int32_t *plist,
                                                   int nrows) {
-    __shared__ double red[NTA];
+    __shared__ double red[NTR];
     const int row = grid_row();
     if (row >= nrows) return;
     const int p = plist ? plist[row] : row;
@@ -801,7 +801,7 @@ __global__ void __launch_bounds__(NTA) k_derefine(mlamr_level ol, mlamr_level pa
     double dsum[M];
 #pragma unroll
     for (int m = 0; m < M; ++m) dsum[m] = 0.0;
-    for (int idx = blockIdx.x * NTA + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTA) {
+    for (int idx = blockIdx.x * NTR + threadIdx.x; idx < cnx * cny; idx += gridDim.x * NTR) {
         const int J = idx / cnx, I = idx % cnx;
         const int ci = clo_i + I, cj = clo_j + J;
         if (owner_at(new_child, par.level_nx, par.level_ny, ci, cj) >= 0) continue;
@@ -823,7 +823,7 @@ __global__ void __launch_bounds__(NTA) k_derefine(mlamr_level ol, mlamr_level pa
     }
 #pragma unroll
     for (int m = 0; m < M; ++m) {
-        const double s = block_sum<NTA>(dsum[m], red);
+        const double s = block_sum<NTR>(dsum[m], red);
         if (threadIdx.x == 0) delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = s;
     }
 }
@@ -1271,8 +1271,14 @@ extern "C" int mlamr_regrid_fill(mlamr_level newlv, mlamr_level oldlv, mlamr_lev
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_regrid_fill<M><<<grid, NTA, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status,
-                                               patch_list, nb);
+        // one block per patch (small patches, e.g. C5's 16x16): 64 threads,
+        // so a patch's few cells do not leave most of a block idle
+        if (blocks_per_patch == 1)
+            k_regrid_fill<M, 64><<<grid, 64, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status,
+                                                      patch_list, nb);
+        else
+            k_regrid_fill<M><<<grid, NTA, 0, st>>>(newlv, oldlv, parent, r_x, r_y, prm, refine_delta, status,
+                                                   patch_list, nb);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();
@@ -1287,7 +1293,11 @@ extern "C" int mlamr_derefine_delta(mlamr_level oldlv, mlamr_level parent, const
     cudaStream_t st = as_stream(stream);
     int rc = dispatch_m(prm.num_layers, [&](auto Mc) {
         constexpr int M = decltype(Mc)::value;
-        k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta, patch_list, nb);
+        if (blocks_per_patch == 1)
+            k_derefine<M, 64><<<grid, 64, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta, patch_list,
+                                                   nb);
+        else
+            k_derefine<M><<<grid, NTA, 0, st>>>(oldlv, parent, new_child, r_x, r_y, derefine_delta, patch_list, nb);
     });
     if (rc) return rc;
     return (int)cudaGetLastError();

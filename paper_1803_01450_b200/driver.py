@@ -337,7 +337,10 @@ class Simulation:
             return
         # a few blocks per patch, each thread over ~8 cells: the per-block
         # reduction, not the bytes, had dominated with one cell per thread
-        bpp = max(1, min(64, -(-pool.max_cells // (8 * 256))))
+        # (up to 1024 blocks for a level of a few large patches, e.g. a
+        # 1280^2 level 1: 64 blocks left most of the GPU idle)
+        cap = 64 if pool.P >= 64 else 1024
+        bpp = max(1, min(cap, -(-pool.max_cells // (8 * 256))))
         with torch.cuda.stream(self.stream):
             part = self._scratch("reduce", pool.P * bpp * self.M)
             ghosts = pool.state if pool.ghosts_in_cur else pool.other

@@ -15,7 +15,7 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 pb = problems.CONFIGS[name]()
 st = torch.cuda.Stream()
 sim = Simulation(pb, stream=st)
-for _ in range(2):
+for _ in range(1 if name == "C5s" else 2):   # C5s meets the CFL guard in its 4th step
     bench.coarse_step(sim)
 sim.kernel_timer = {}
 torch.cuda.synchronize()
