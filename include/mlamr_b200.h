@@ -168,6 +168,7 @@ int mlamr_step_finalize(mlamr_level lv, const double *src_state, double *dst_sta
  * + s_c, and acc2[c] += s_c when acc2 is given.  One launch in place of the
  * framework reductions the driver used for mass and refine/derefine
  * deltas. */
+int mlamr_memset(void *ptr, int byte, long long nbytes, void *stream);  /* cudaMemsetAsync */
 int mlamr_sum_partials(const double *part, long long rows, int cols, double scale, double *acc,
                        double *acc2, int init, void *stream);
 

@@ -1799,6 +1799,13 @@ extern "C" int mlamr_flags_finish(const uint8_t *raw, const uint8_t *covered, in
     return (int)cudaGetLastError();
 }
 
+// Byte fill of device memory (cudaMemsetAsync: a copy-engine memset, not a
+// kernel): zero planes, -1 (0xff) owner maps and "all dry" speed bits.
+extern "C" int mlamr_memset(void *ptr, int byte, long long nbytes, void *stream) {
+    if (nbytes <= 0) return 0;
+    return (int)cudaMemsetAsync(ptr, byte, (size_t)nbytes, as_stream(stream));
+}
+
 extern "C" int mlamr_version(void) { return 1; }
 
 extern "C" const char *mlamr_build_info(void) {

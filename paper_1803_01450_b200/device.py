@@ -85,6 +85,23 @@ ALLOC_STATS = {"fresh": 0, "fresh_bytes": 0, "reused": 0}
 POOL_PROF = __import__("collections").defaultdict(float)   # host seconds inside LevelPool()
 
 
+def dmemset(t: torch.Tensor, byte: int, stream) -> torch.Tensor:
+    """Fill a contiguous device tensor with one byte value on ``stream``
+    (cudaMemsetAsync, not a kernel): 0 for zero planes, 0xff for -1."""
+    n = t.numel() * t.element_size()
+    if n:
+        rc = N.lib().mlamr_memset(t.data_ptr(), int(byte), n, _stream_handle(stream))
+        if rc:
+            raise N.NativeLibraryError(f"memset failed (cuda error {rc})")
+    return t
+
+
+def dzeros(n: int, dtype, device, stream) -> torch.Tensor:
+    with torch.cuda.stream(stream):
+        t = torch.empty(n, dtype=dtype, device=device)
+    return dmemset(t, 0, stream)
+
+
 def acquire(numel: int, dtype, device, stream) -> torch.Tensor:
     device = torch.device(device)
     if device.type == "cuda" and device.index is None:
@@ -231,7 +248,7 @@ class LevelPool:
             _t1 = _t.perf_counter()
             _p["acquire"] += _t1 - _t0
             for t in (self.buf[0], self.buf[1], self.bathy):
-                t.zero_()
+                dmemset(t, 0, stream)
             _t2 = _t.perf_counter()
             _p["zero"] += _t2 - _t1
             A = arena()
@@ -249,13 +266,12 @@ class LevelPool:
             if self.owned is not None:
                 ol = np.flatnonzero(self.owned).astype(np.int32)
                 self.n_owned = len(ol)
-                self.owned_d = A.upload(ol, device, stream) if len(ol) else \
-                    torch.zeros(1, dtype=torch.int32, device=device)
-            self.speed_bits = torch.full((max(self.P, 1),), -1, dtype=torch.int64, device=device)
+                self.owned_d = A.upload(ol, device, stream) if len(ol) else dzeros(1, torch.int32, device, stream)
+            self.speed_bits = dmemset(torch.empty(max(self.P, 1), dtype=torch.int64, device=device), 0xFF, stream)
             mapn = (spec.nx + 2 * GHOST_WIDTH) * (spec.ny + 2 * GHOST_WIDTH)
             _t4 = _t.perf_counter()
-            self.own = acquire(mapn, torch.int32, device, stream).fill_(-1)
-            self.gown = acquire(mapn, torch.int32, device, stream).fill_(-1) if need_gown else None
+            self.own = dmemset(acquire(mapn, torch.int32, device, stream), 0xFF, stream)
+            self.gown = dmemset(acquire(mapn, torch.int32, device, stream), 0xFF, stream) if need_gown else None
             _p["maps"] += _t.perf_counter() - _t4
         self.child: Optional[torch.Tensor] = None   # finer level's coarsened owner map
         self.cur = 0
@@ -279,8 +295,8 @@ class LevelPool:
             tl = tl[self.owned[tl[:, 0]]]
         with torch.cuda.stream(self.stream):
             td = arena().upload(tl, self.device, self.stream) if len(tl) else \
-                torch.zeros(3, dtype=torch.int32, device=self.device)
-            acc = torch.zeros(max(len(tl), 1) * (self.M + 2), dtype=torch.float64, device=self.device)
+                dzeros(3, torch.int32, self.device, self.stream)
+            acc = dzeros(max(len(tl), 1) * (self.M + 2), torch.float64, self.device, self.stream)
         self._tiles = (tl, len(tl), td, acc)
         POOL_PROF["tile_list"] += _t.perf_counter() - t0
 
@@ -365,7 +381,7 @@ class LevelPool:
             # round trip for their count (n_cells is the list's capacity)
             cap = max(total, 1)
             cells = torch.empty(2 * cap, dtype=torch.int32, device=self.device)
-            count = torch.zeros(1, dtype=torch.int32, device=self.device)
+            count = dzeros(1, torch.int32, self.device, self.stream)
             if self.owned is not None:
                 pl, nl = (self.owned_d.data_ptr(), self.n_owned) if self.n_owned else (None, 0)
             else:
@@ -380,8 +396,8 @@ class LevelPool:
         if self.owned is not None:
             touch &= self.owned
         bcp = np.flatnonzero(touch).astype(np.int32)
-        bc_d = A.upload(bcp, self.device, self.stream) if len(bcp) else torch.zeros(1, dtype=torch.int32,
-                                                                                     device=self.device)
+        bc_d = A.upload(bcp, self.device, self.stream) if len(bcp) else dzeros(1, torch.int32, self.device,
+                                                                                self.stream)
         self._plan = (gbase_d, plan, cells, cap if nl else 0, bc_d, len(bcp), int(ng.max()) if len(ng) else 0)
         return self._plan
 
@@ -531,7 +547,7 @@ def paint_child_map(parent_spec: LevelSpec, fine_boxes: np.ndarray, rx: int, ry:
     footprints (coverage_mask, mesh.py:271-279)."""
     mapn = (parent_spec.nx + 2 * GHOST_WIDTH) * (parent_spec.ny + 2 * GHOST_WIDTH)
     with torch.cuda.stream(stream):
-        m = acquire(mapn, torch.int32, device, stream).fill_(-1)
+        m = dmemset(acquire(mapn, torch.int32, device, stream), 0xFF, stream)
         if len(fine_boxes):
             bd = arena().upload(np.asarray(fine_boxes, np.int32).reshape(-1, 4), device, stream)
             nx = fine_boxes[:, 2] - fine_boxes[:, 0] + 1

@@ -37,7 +37,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import LevelPool, acquire, arena, empty_level_struct, paint_child_map, release
+from .device import LevelPool, acquire, arena, dmemset, dzeros, empty_level_struct, paint_child_map, release
 from .errors import CflViolationError, NumericalAbortError, TimeSyncError, raise_status
 from .mesh import GHOST_WIDTH, IndexBox, LevelSpec, boxes_array, paint
 from .regrid import chop_boxes, cluster_boxes, cluster_boxes_device, nesting_allowed
@@ -246,8 +246,7 @@ class Simulation:
             self._scratch_bufs[name] = buf
         out = buf[:max(n, 1)]
         if zero:
-            with torch.cuda.stream(self.stream):
-                out.zero_()
+            dmemset(out, 0, self.stream)
         return out
 
     def spec(self, level: int) -> LevelSpec:
@@ -467,7 +466,7 @@ class Simulation:
         if buf is None:
             with torch.cuda.stream(self.stream):
                 buf = {
-                    "bits": torch.zeros(n, dtype=torch.uint8, device=self.dev),
+                    "bits": dzeros(n, torch.uint8, self.dev, self.stream),
                     "scratch": torch.empty(3 * n, dtype=torch.uint8, device=self.dev),
                     "flags": torch.empty(n, dtype=torch.uint8, device=self.dev),
                     "allowed": torch.empty(n, dtype=torch.uint8, device=self.dev),
@@ -557,7 +556,7 @@ class Simulation:
                     b["allowed"].mul_(region)
             return b["flags"], b["allowed"]
         with torch.cuda.stream(self.stream):
-            b["bits"].zero_()
+            dmemset(b["bits"], 0, self.stream)
             pl, nl = pool.work_list()
             if pool.P and (pl is None or nl > 0):
                 self._call(self.lib.mlamr_flag_cells, pool.struct(), pool.state.data_ptr(), self.prm,
@@ -784,7 +783,7 @@ class Simulation:
         with torch.cuda.stream(self.stream):
             bits_h = self._pinned("speed", pool.P, torch.int64)
             bits_h.copy_(pool.speed_bits[:pool.P], non_blocking=True)
-            pool.speed_bits.fill_(-1)   # back to "all dry" for the next step
+            dmemset(pool.speed_bits, 0xFF, self.stream)   # back to "all dry" (-1) for the next step
         return bits_h
 
     def level_speed(self, level: int) -> float:

@@ -32,7 +32,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
-from .device import LevelPool, empty_level_struct, paint_child_map
+from .device import LevelPool, dmemset, empty_level_struct, paint_child_map
 from .distributed import (Comm, Transfer, _any_meet, needed, partition, patch_sizes, plan_acquire, plan_refresh,
                           ring_segments, run_transfer)
 from .driver import Simulation
@@ -324,14 +324,14 @@ class ShardedSimulation(Simulation):
         with torch.cuda.stream(self.stream):
             best = torch.full((1,), -1, dtype=torch.int64, device=self.dev)
             if pool is not None and pool.P:
-                pool.speed_bits.fill_(-1)
+                dmemset(pool.speed_bits, 0xFF, self.stream)
                 if pool.n_tiles:
                     self._call(self.lib.mlamr_max_speed_tiles, pool.struct(), pool.state.data_ptr(),
                                pool.tiles_d.data_ptr(), pool.n_tiles, pool.tile_tx, self.prm,
                                pool.speed_bits.data_ptr(),
                                self.sh)
                 best = torch.max(pool.speed_bits[:pool.P]).reshape(1)
-                pool.speed_bits.fill_(-1)   # back to "all dry" for the next step (see the driver)
+                dmemset(pool.speed_bits, 0xFF, self.stream)   # back to "all dry" for the next step (see the driver)
             self.comm.allreduce(best, dist.ReduceOp.MAX if self.world > 1 else None)
         self.stream.synchronize()
         b = int(best.item())
@@ -402,7 +402,7 @@ class ShardedSimulation(Simulation):
                            float(tol), owned.data_ptr(), b["bits"].data_ptr(), b["scratch"].data_ptr(),
                            self._flagbuf[key].data_ptr(), self.sh)
             else:
-                b["bits"].zero_()
+                dmemset(b["bits"], 0, self.stream)
             self._reduce_flag_bits(b["bits"])          # union of the ranks' owned flags
             cov = arena().upload(paint(self.layout[level], s.ny, s.nx).astype(np.uint8).reshape(-1),
                                  self.dev, self.stream)
@@ -483,7 +483,7 @@ class ShardedSimulation(Simulation):
                 self._set_initial(new)
             elif new.P:
                 bpp = new.blocks_per_patch(new.max_interior // 4)   # copy pass: ~4 fine cells per thread
-                part = torch.zeros(new.P * bpp * M, dtype=torch.float64, device=self.dev)
+                part = self._scratch("refine", new.P * bpp * M)
                 ol = old.struct() if old is not None else empty_level_struct(self.spec(level + 1), M)
                 pl, nl = new.work_list()
                 if nl > 0:
@@ -494,7 +494,7 @@ class ShardedSimulation(Simulation):
             new_child = paint_child_map(s, nboxes, rx, ry, self.dev, self.stream)
             if old is not None and old.P and not init:
                 bpp = old.blocks_per_patch(old.max_interior // (rx * ry))
-                part = torch.zeros(old.P * bpp * M, dtype=torch.float64, device=self.dev)
+                part = self._scratch("derefine", old.P * bpp * M)
                 pl, nl = old.work_list()
                 if nl > 0:
                     self._call(self.lib.mlamr_derefine_delta, old.struct(), par.struct(), new_child.data_ptr(),
