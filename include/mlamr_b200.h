@@ -169,6 +169,9 @@ int mlamr_step_finalize(mlamr_level lv, const double *src_state, double *dst_sta
  * framework reductions the driver used for mass and refine/derefine
  * deltas. */
 int mlamr_memset(void *ptr, int byte, long long nbytes, void *stream);  /* cudaMemsetAsync */
+/* Host: the step tile list (patch, j0, i0) of int64 boxes [n][4] for tiles
+ * of tile_y x tile_x, patch-major; returns the count (out NULL: count only). */
+long long mlamr_tile_list(const int64_t *boxes, int n, int tile_y, int tile_x, int32_t *out);
 int mlamr_sum_partials(const double *part, long long rows, int cols, double scale, double *acc,
                        double *acc2, int init, void *stream);
 

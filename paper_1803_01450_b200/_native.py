@@ -67,6 +67,7 @@ SIGNATURES = {
                                   ctypes.c_int, Params, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "mlamr_step_finalize": (ctypes.c_int, [Level, c_vp, c_vp, c_vp, ctypes.c_int, ctypes.c_double,
                                            Params, c_vp, c_vp, c_vp, c_vp, c_vp, ctypes.c_int, c_vp]),
+    "mlamr_tile_list": (ctypes.c_longlong, [c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp]),
     "mlamr_memset": (ctypes.c_int, [c_vp, ctypes.c_int, ctypes.c_longlong, c_vp]),
     "mlamr_sum_partials": (ctypes.c_int, [c_vp, ctypes.c_longlong, ctypes.c_int, ctypes.c_double, c_vp, c_vp,
                                           ctypes.c_int, c_vp]),

@@ -296,6 +296,28 @@ extern "C" int mlamr_chop_boxes(const int32_t *boxes, int n, int max_nx, int max
     return (int)res.size();
 }
 
+// Step tile list (device.tile_list): (patch, j0, i0) for every tile_y x
+// tile_x interior tile of every box, patch-major, rows of tiles in order.
+// Returns the count; out may be NULL to count only.
+extern "C" long long mlamr_tile_list(const int64_t *boxes, int n, int tile_y, int tile_x, int32_t *out) {
+    long long t = 0;
+    for (int p = 0; p < n; ++p) {
+        const int64_t nx = boxes[4 * p + 2] - boxes[4 * p] + 1, ny = boxes[4 * p + 3] - boxes[4 * p + 1] + 1;
+        const int tx = (int)((nx + tile_x - 1) / tile_x), ty = (int)((ny + tile_y - 1) / tile_y);
+        if (out != nullptr)
+            for (int a = 0; a < ty; ++a)
+                for (int b = 0; b < tx; ++b) {
+                    out[3 * t] = p;
+                    out[3 * t + 1] = a * tile_y;
+                    out[3 * t + 2] = b * tile_x;
+                    ++t;
+                }
+        else
+            t += (long long)tx * ty;
+    }
+    return t;
+}
+
 // For each box of `a` (int64 [na][4], inclusive), does it intersect any box
 // of `b`?  Bucket grid over b's extent (cell `bucket`), CSR of box ids per
 // bucket, exact tests on candidates.  Host-side planning for multi-GPU

@@ -401,9 +401,9 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
 #pragma unroll
     for (int it = 0; it < (NEXT ? MAXIT : 1); ++it) k2s[it] = -1;
     const unsigned char *CWc = cowet_pl<M, SW>(s);
-#pragma unroll
     const int uw = uc1 - uc0;
     const unsigned um = c_div_magic[uw];
+#pragma unroll
     for (int it = 0; it < MAXIT; ++it) {
         const int idx_ = threadIdx.x + it * NT;
         if (idx_ >= (ur1 - ur0) * uw) break;

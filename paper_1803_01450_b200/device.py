@@ -195,18 +195,12 @@ def tile_list(boxes: np.ndarray, shape: Optional[tuple] = None) -> np.ndarray:
     if shape is None:
         shape = N.step_tile(int((boxes[:, 2] - boxes[:, 0] + 1).max()), 2)
     TILE_Y, TILE_X = shape
-    nx = boxes[:, 2] - boxes[:, 0] + 1
-    ny = boxes[:, 3] - boxes[:, 1] + 1
-    tx = (nx + TILE_X - 1) // TILE_X
-    ty = (ny + TILE_Y - 1) // TILE_Y
-    cnt = tx * ty
-    p = np.repeat(np.arange(len(boxes)), cnt)
-    start = np.concatenate([[0], np.cumsum(cnt)[:-1]])
-    k = np.arange(cnt.sum()) - np.repeat(start, cnt)
-    txr = np.repeat(tx, cnt)
-    j0 = (k // txr) * TILE_Y
-    i0 = (k % txr) * TILE_X
-    return np.stack([p, j0, i0], axis=1).astype(np.int32)
+    b = np.ascontiguousarray(boxes, dtype=np.int64).reshape(-1, 4)
+    L = N.lib()
+    n = int(L.mlamr_tile_list(b.ctypes.data, len(b), int(TILE_Y), int(TILE_X), None))
+    out = np.empty((n, 3), np.int32)
+    L.mlamr_tile_list(b.ctypes.data, len(b), int(TILE_Y), int(TILE_X), out.ctypes.data)
+    return out
 
 
 class LevelPool:
