@@ -294,6 +294,17 @@ class LevelPool:
         self._tiles = (tl, len(tl), td, acc)
         POOL_PROF["tile_list"] += _t.perf_counter() - t0
 
+    def reorder_tiles(self, order: np.ndarray) -> None:
+        """Permute the step work list (per-tile partials follow the list)."""
+        if self._tiles is None:
+            self._build_tiles()
+        tl, n, _, acc = self._tiles
+        tl = np.ascontiguousarray(tl[np.asarray(order, np.int64)])
+        with torch.cuda.stream(self.stream):
+            td = arena().upload(tl, self.device, self.stream) if len(tl) else \
+                dzeros(3, torch.int32, self.device, self.stream)
+        self._tiles = (tl, n, td, acc)
+
     @property
     def tiles(self) -> np.ndarray:
         if self._tiles is None:

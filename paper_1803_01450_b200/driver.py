@@ -388,12 +388,15 @@ class Simulation:
         return out.numpy().copy()
 
     # -- ghost filling (driver.py:157-190) ------------------------------------
-    def fill_level_ghosts(self, level: int, t: float, siblings: bool = True) -> None:
+    def fill_level_ghosts(self, level: int, t: float, siblings: bool = True, part: str = "all") -> None:
         """Ghost frames of a level at time t (driver.py:175-190).  With
         ``siblings=False`` the sibling copies are left to the step that
         follows (mlamr_step reads sibling halo cells through the ghost plan);
         only patches with physical BCs get them, because their BC corners
-        read the copied frame."""
+        read the copied frame.  ``part`` (with siblings=False) splits that
+        fill: "interp" = the parent-interpolated cells only, "bc" = the BC
+        patches' sibling copies and boundary conditions only (the sharded
+        driver runs them on either side of a shadow exchange)."""
         pool = self.levels[level]
         if pool.P == 0:
             return
@@ -425,6 +428,10 @@ class Simulation:
             pl, nl = pool.work_list()
         else:
             pl, nl = bc_d.data_ptr(), n_bc
+        if not siblings and part == "interp":
+            nl, n_bc = 0, 0
+        elif not siblings and part == "bc":
+            n_cells = 0
         timed = not siblings and level > 1 and n_cells
         e0 = self._kt0() if timed else None
         self._call(self.lib.mlamr_fill_ghosts_planned, pool.struct(), par_ptr, old_ptr, theta, rx, ry, self.bcs,
@@ -690,7 +697,10 @@ class Simulation:
         self.host_prof["regrid(total)"] += time.perf_counter() - t0
 
     # -- stepping (driver.py:224-309) ------------------------------------------------
-    def _step_patches(self, level: int, dt: float, fused_siblings: bool = False) -> None:
+    def _step_patches(self, level: int, dt: float, fused_siblings: bool = False, split=None) -> None:
+        """``split`` = (n_first, between): step the first n_first tiles of the
+        level's tile list, call ``between()`` (which may enqueue work and
+        stream waits), then step the rest; one finalize over all tiles."""
         pool = self.levels[level]
         if pool.P == 0:
             return
@@ -714,9 +724,18 @@ class Simulation:
         if fused_siblings:
             gbase, plan = pool.ghost_plan()[:2]
             gb, gp = gbase.data_ptr(), plan.data_ptr()
-        self._call(self.lib.mlamr_step, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr(),
-                   pool.n_tiles, pool.tile_tx, dt, y_first, self.prm, pool.speed_bits.data_ptr(), pool.tile_acc.data_ptr(),
-                   self.status.data_ptr(), gb, gp, self.sh)
+        if split is None:
+            parts = [(0, pool.n_tiles)]
+        else:
+            parts = [(0, split[0]), (split[0], pool.n_tiles)]
+        for k, (a, b) in enumerate(parts):
+            if k == 1:
+                split[1]()
+            if b <= a:
+                continue
+            self._call(self.lib.mlamr_step, lv, src.data_ptr(), dst.data_ptr(), pool.tiles_d.data_ptr() + 12 * a,
+                       b - a, pool.tile_tx, dt, y_first, self.prm, pool.speed_bits.data_ptr(),
+                       pool.tile_acc.data_ptr() + 8 * (self.M + 2) * a, self.status.data_ptr(), gb, gp, self.sh)
         if timed:
             e1.record(self.stream)
             self.step_events.append((e0, e1, pool))

@@ -521,7 +521,38 @@ class ShardedSimulation(Simulation):
         return True
 
     # -- recursion with refresh points -------------------------------------------------
+    def _split_tiles(self, level: int) -> int:
+        """Order the finest level's tiles so that those whose step reads no
+        shadow (no halo cell inside a foreign sibling, patch not touching the
+        level box, whose BC corners read copied cells) come first; returns
+        their number (cached per pool and layout)."""
+        pool = self.levels[level]
+        key = (id(pool), pool.n_tiles)
+        if getattr(pool, "_split_key", None) == key:
+            return pool._n_indep
+        tl = pool.tiles
+        b = pool.boxes
+        ty, tx = pool.tile_shape
+        p = tl[:, 0]
+        lo_i = b[p, 0] + tl[:, 2]
+        lo_j = b[p, 1] + tl[:, 1]
+        pad = np.stack([lo_i - 1, lo_j - 1, np.minimum(lo_i + tx - 1, b[p, 2]) + 1,
+                        np.minimum(lo_j + ty - 1, b[p, 3]) + 1], axis=1)
+        shadows = b[~pool.owned] if pool.owned is not None else _EMPTY
+        dep = _any_meet(pad, shadows) if len(shadows) else np.zeros(len(tl), bool)
+        s = self.spec(level)
+        touch = (b[:, 0] == 0) | (b[:, 2] == s.nx - 1) | (b[:, 1] == 0) | (b[:, 3] == s.ny - 1)
+        dep = dep | touch[p]
+        pool.reorder_tiles(np.concatenate([np.flatnonzero(~dep), np.flatnonzero(dep)]))
+        pool._split_key = (id(pool), pool.n_tiles)
+        pool._n_indep = int((~dep).sum())
+        return pool._n_indep
+
     def advance_level(self, level: int, dt: float, t0: float) -> None:
+        if (self.overlap_refresh and self.world > 1 and level == self.L and self.fuse_sibling_fill
+                and level in self.levels and self.levels[level].P):
+            self._advance_finest_overlapped(level, dt, t0)
+            return
         self._refresh(level)                                            # (i)
         if level < self.L and self.steps[level] % self.pb.regrid_interval == 0:
             self.regrid_from(level)
@@ -564,6 +595,29 @@ class ShardedSimulation(Simulation):
             self._refresh(level + 1, coarsen=True)                      # (iv)
             self._average_down(level)
             del self._stash[level]
+
+    def _advance_finest_overlapped(self, level: int, dt: float, t0: float) -> None:
+        """The finest level with its shadow refresh (i) on the exchange stream:
+        the parent-interpolated part of the fill and the tiles whose step
+        reads no shadow run while the exchange is in flight; the BC patches'
+        fill and the remaining tiles wait for it.  Same arithmetic as the
+        sequential order (the two parts write disjoint cells)."""
+        n1 = self._split_tiles(level)
+        self._xstream.wait_stream(self.stream)
+        self._refresh(level, stream=self._xstream)                     # (i)
+        ev = torch.cuda.Event()
+        ev.record(self._xstream)
+        self.fill_level_ghosts(level, t0, siblings=False, part="interp")
+        self.levels[level].fused_frame = True
+
+        def between():
+            self.stream.wait_event(ev)
+            self.fill_level_ghosts(level, t0, siblings=False, part="bc")
+
+        pool = self.levels[level]
+        self._step_patches(level, dt, fused_siblings=True, split=(n1, between))
+        self.steps[level] += 1
+        pool.time = t0 + dt
 
     def owned_fields(self, level: int):
         """{global index: (box, h, hu, hv, bathy)} of this rank's patches."""

@@ -110,6 +110,12 @@ def main():
     assert c.total_cell_updates == b.total_cell_updates and c.cell_updates_per_level == b.cell_updates_per_level
     assert c.refine_delta == b.refine_delta and c.clipped_mass == b.clipped_mass
     np.testing.assert_allclose(sh.composite_mass(), ref.composite_mass(), rtol=1e-12)
+    if sh.overlap_refresh:
+        # the finest level ran its refresh (i) overlapped: some tiles before
+        # the exchange completed, the rest after it
+        fp = sh.levels[sh.L]
+        assert 0 < fp._n_indep < fp.n_tiles, (fp._n_indep, fp.n_tiles)
+        print(f"rank {rank}: finest tiles stepped during the exchange {fp._n_indep} of {fp.n_tiles}", flush=True)
     print(f"rank {rank}: {name} sharded == single-GPU ({steps} steps, exchanged {sh.bytes_exchanged} B, "
           f"owned {[int(p.n_owned) for p in sh.levels.values()]} of {[len(v) for v in sh.layout.values()]})",
           flush=True)
