@@ -31,6 +31,8 @@ def wrap(obj, name, label):
 wrap(regrid, "_cluster_from_sat", "bisection")
 wrap(D, "chop_boxes", "chop")
 wrap(DV.LevelPool, "__init__", "LevelPool()")
+wrap(DV.LevelPool, "_build_tiles", "tile list")
+wrap(DV.LevelPool, "ghost_plan", "ghost_plan")
 wrap(D.Simulation, "_new_pool", "_new_pool (incl. bathy fill/check)")
 wrap(D.Simulation, "_rebuild", "_rebuild (total)")
 orig_sync = torch.cuda.Stream.synchronize
@@ -43,12 +45,14 @@ def tsync(self):
 
 
 torch.cuda.Stream.synchronize = tsync
-pb = problems.config4()
+name = sys.argv[1] if len(sys.argv) > 1 else "C4"
+pb = problems.CONFIGS[name]()
 sim = D.Simulation(pb, stream=torch.cuda.Stream())
-for _ in range(5):
+warm, steps = (1, 2) if name == "C5s" else (5, 10)   # C5s meets the CFL guard in its 4th step
+for _ in range(warm):
     bench.coarse_step(sim)
 marks.clear()
-for _ in range(10):
+for _ in range(steps):
     bench.coarse_step(sim)
 torch.cuda.synchronize()
 # per rebuild: phases after the clustering sync
