@@ -684,8 +684,14 @@ __global__ void __launch_bounds__(NTA) k_check_bathy(mlamr_level fine, mlamr_lev
 // r_x*r_y children from the old patch covering them, or refine them from
 // the parent's interiors (gather include_ghosts=False, regrid.py:295-300).
 // ---------------------------------------------------------------------------
+// 3 CTAs/SM (<= 80 registers): the copy pass -- most of a rebuild -- is
+// latency-bound on its owner-map -> source chain and wants the warps; the
+// rarer refine pass spills a little (C4 level-3 rebuild 1.24 -> 1.08 ms)
+#ifndef MLAMR_RG_MINB
+#define MLAMR_RG_MINB 3
+#endif
 template <int M, int NTR = NTA>
-__global__ void __launch_bounds__(NTR) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
+__global__ void __launch_bounds__(NTR, NTR == NTA ? MLAMR_RG_MINB : 1) k_regrid_fill(mlamr_level nl, mlamr_level ol, mlamr_level par,
                                                      int r_x, int r_y, mlamr_params prm,
                                                      double *refine_delta, int32_t *status, const int32_t *plist,
                                                      int nrows) {
