@@ -83,11 +83,17 @@ __constant__ unsigned c_div_magic[64] = {
 #undef MLAMR_STEP_NT
 #undef MLAMR_STEP_MINB
 
+#ifndef MLAMR_N_NT
+#define MLAMR_N_NT 192
+#endif
+#ifndef MLAMR_N_MINB
+#define MLAMR_N_MINB 4
+#endif
 #define MLAMR_STEP_NS narrow
 #define MLAMR_STEP_TX 16
 #define MLAMR_STEP_TY 16
-#define MLAMR_STEP_NT 192
-#define MLAMR_STEP_MINB 4
+#define MLAMR_STEP_NT MLAMR_N_NT
+#define MLAMR_STEP_MINB MLAMR_N_MINB
 #include "step_tile.cuh"
 #undef MLAMR_STEP_NS
 #undef MLAMR_STEP_TX
@@ -207,6 +213,9 @@ extern "C" int mlamr_step_tile(int max_patch_nx, int num_layers, int *ty, int *t
     // narrow tiles for narrow patches, and for M >= 3, whose 3M+1 state
     // planes and per-layer scratch make a wide tile's shared memory
     // (~132 KB) allow one CTA per SM (narrow: ~70 KB, 3 CTAs)
+#ifdef MLAMR_FORCE_NARROW
+    max_patch_nx = 1;
+#endif
     if ((max_patch_nx > 0 && max_patch_nx <= narrow::TX) || num_layers >= 3) {
         *ty = narrow::TY;
         *tx = narrow::TX;
