@@ -1436,8 +1436,10 @@ __global__ void k_selftest_div(const double *a, const double *b, int n, unsigned
         const double r = recip_nr(y);
         const double q = div_fast(x, y, r, ok);
         const double ref = x / y;
+        // the kernels' fallback for a refused division must be `/` too
+        const double got = ok ? q : div_slow(x, y);
         if (!ok) atomicAdd(slow, 1ull);
-        else if (__double_as_longlong(q) != __double_as_longlong(ref) && !(q != q && ref != ref))
+        if (__double_as_longlong(got) != __double_as_longlong(ref) && !(got != got && ref != ref))
             atomicAdd(bad, 1ull);
     }
 }

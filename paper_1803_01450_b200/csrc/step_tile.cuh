@@ -124,10 +124,10 @@ __device__ __forceinline__ void post_cell(double (&h)[M], double (&hu)[M], doubl
             double u1 = div_fast(hu1, h1, y1, ok), v1 = div_fast(hv1, h1, y1, ok);
             double u2 = div_fast(hu2, h2, y2, ok), v2 = div_fast(hv2, h2, y2, ok);
             if (!ok) {
-                u1 = hu1 / h1;
-                u2 = hu2 / h2;
-                v1 = hv1 / h1;
-                v2 = hv2 / h2;
+                u1 = div_slow(hu1, h1);
+                u2 = div_slow(hu2, h2);
+                v1 = div_slow(hv1, h1);
+                v2 = div_slow(hv2, h2);
             }
             const double du = u1 - u2, dv = v1 - v2;
             const double shear2 = (du * du) + (dv * dv);
@@ -251,8 +251,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     u = div_fast(hn, h[m], y, ok);
                     v = div_fast(ht, h[m], y, ok);
                     if (!ok) {
-                        u = hn / h[m];
-                        v = ht / h[m];
+                        u = div_slow(hn, h[m]);
+                        v = div_slow(ht, h[m]);
                     }
                 }
                 s.u[m][k] = u;
@@ -335,8 +335,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     fh = div_fast(nh, den, y, ok);
                     fm = div_fast(nm, den, y, ok);
                     if (!ok) {
-                        fh = nh / den;
-                        fm = nm / den;
+                        fh = div_slow(nh, den);
+                        fm = div_slow(nm, den);
                     }
                 }
             }
@@ -362,7 +362,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     const double dp = wp ? f[kp] - f[k] : 0.0;
                     const double num = ((-g) * s.S[m][k]) * (0.5 * (dp + dm));
                     double q = div_fast(num, d, yd, ok);
-                    if (!ok) q = num / d;
+                    if (!ok) q = div_slow(num, d);
                     acc = q;
                     has = true;
                 }
@@ -374,7 +374,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     const double num = (((-rr[kk][m]) * g) * s.S[m][k]) * (0.5 * (dp + dm));
                     ok = true;
                     double q = div_fast(num, d, yd, ok);
-                    if (!ok) q = num / d;
+                    if (!ok) q = div_slow(num, d);
                     acc = has ? acc + q : q;
                     has = true;
                 }
@@ -461,7 +461,7 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     const double num = ((-g) * h0) * (0.5 * (dp + dm));
                     bool ok = true;
                     sm = div_fast(num, d, yd, ok);
-                    if (!ok) sm = num / d;
+                    if (!ok) sm = div_slow(num, d);
                 } else {
                     sm = src_pl<M, SW>(s, m - 1)[k];
                 }
@@ -509,8 +509,8 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                     u = div_fast(nt[m], nh[m], y, ok);
                     v = div_fast(nn[m], nh[m], y, ok);
                     if (!ok) {
-                        u = nt[m] / nh[m];
-                        v = nn[m] / nh[m];
+                        u = div_slow(nt[m], nh[m]);
+                        v = div_slow(nn[m], nh[m]);
                     }
                 }
                 s.u[m][k] = u;
