@@ -38,6 +38,33 @@ struct StepConst {
     double coef;          // g * (1 - rho_0 / rho_1), the shear bound (physics.py:306)
 };
 
+// One tile of the step's work list as the kernel wants it: everything the
+// tile header would otherwise read through the chain tile list ->
+// box/offset -> ghost base (two dependent L2 round trips in front of every
+// CTA's staging; 4.5 % of the kernel's warp-stall samples).  Written by
+// k_make_desc in front of each step launch (~2 us).
+struct __align__(16) TileDesc {
+    int32_t p, tj0, ti0;  // patch, tile origin in the patch interior
+    int32_t nxy;          // patch interior nx | ny << 16
+    int64_t off;          // patch offset in a field plane
+    int64_t gb;           // ghost plan base of the patch (0 without a plan)
+};
+
+__global__ void k_make_desc(mlamr_level lv, const int32_t *__restrict__ tiles, int n_tiles,
+                            const int64_t *__restrict__ gbase, TileDesc *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_tiles) return;
+    TileDesc d;
+    d.p = tiles[3 * i];
+    d.tj0 = tiles[3 * i + 1];
+    d.ti0 = tiles[3 * i + 2];
+    const int32_t *b = lv.box + 4 * d.p;
+    d.nxy = (b[2] - b[0] + 1) | ((b[3] - b[1] + 1) << 16);
+    d.off = lv.offset[d.p];
+    d.gb = gbase != nullptr ? gbase[d.p] : 0;
+    out[i] = d;
+}
+
 // ceil(2^16 / w) for the step's compact rectangle iteration (step_tile.cuh):
 // q = (idx * c_div_magic[w]) >> 16 == idx / w for every idx < 65536 / w.
 __constant__ unsigned c_div_magic[64] = {
@@ -114,6 +141,36 @@ static int step_form_init() {
 }
 static std::atomic<int> g_step_form{step_form_init()};
 static bool use_walker() { return g_step_form.load(std::memory_order_relaxed) == 1; }
+
+// Descriptor scratch, one per (device, stream), grown on demand: launches
+// on one stream are ordered, so reuse is safe.
+static TileDesc *desc_scratch(cudaStream_t st, int n_tiles) {
+    struct Buf { TileDesc *p; int cap; };
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, Buf> pool;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    Buf &b = pool[{dev, st}];
+    if (b.cap < n_tiles) {
+        // the old buffer may still be read by a launch in flight on `st`
+        if (b.p != nullptr) cudaFreeAsync(b.p, st);
+        b.p = nullptr;
+        b.cap = 0;
+        const int cap = n_tiles + n_tiles / 4 + 1024;
+        if (cudaMallocAsync(&b.p, sizeof(TileDesc) * (size_t)cap, st) != cudaSuccess) return nullptr;
+        b.cap = cap;
+    }
+    return b.p;
+}
+
+static const TileDesc *make_desc(const mlamr_level &lv, const int32_t *tiles, int n_tiles, const int64_t *gbase,
+                                 cudaStream_t st) {
+    TileDesc *desc = desc_scratch(st, n_tiles);
+    if (desc != nullptr)
+        k_make_desc<<<(n_tiles + 255) / 256, 256, 0, st>>>(lv, tiles, n_tiles, gbase, desc);
+    return desc;
+}
 
 // CFL guard + deterministic reduction of the step partials.  FIN_BLOCKS
 // CTAs each reduce a fixed contiguous chunk of tiles into chunk[b][q]; the
@@ -232,17 +289,24 @@ static int launch_step_shape(int tile_tx, const mlamr_level &lv, const double *s
                              const mlamr_params &prm, long long *speed_bits, double *tile_acc,
                              const int32_t *status, const int64_t *gbase, const int64_t *gplan,
                              cudaStream_t st) {
-    if (tile_tx == narrow::TX)
-        return narrow::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
-                                      gbase, gplan, st);
+    if (n_tiles <= 0) return 0;
+    if (tile_tx == narrow::TX) {
+        const TileDesc *desc = make_desc(lv, tiles, n_tiles, gbase, st);
+        if (desc == nullptr) return -2;
+        return narrow::launch_step<M>(lv, src, dst, desc, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
+                                      gplan, st);
+    }
     if constexpr (M <= 2) {
         if (tile_tx == wide::TX && use_walker())
             return walk::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc,
                                         status, gbase, gplan, st);
     }
-    if (tile_tx == wide::TX)
-        return wide::launch_step<M>(lv, src, dst, tiles, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
-                                    gbase, gplan, st);
+    if (tile_tx == wide::TX) {
+        const TileDesc *desc = make_desc(lv, tiles, n_tiles, gbase, st);
+        if (desc == nullptr) return -2;
+        return wide::launch_step<M>(lv, src, dst, desc, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
+                                    gplan, st);
+    }
     return -3;
 }
 

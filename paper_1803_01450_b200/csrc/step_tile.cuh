@@ -537,10 +537,9 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
 template <int M, bool YFIRST>
 __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, const double *__restrict__ src,
                                              double *__restrict__ dst,
-                                             const int32_t *__restrict__ tiles, double dt,
+                                             const TileDesc *__restrict__ desc, double dt,
                                              mlamr_params prm, StepConst kc, long long *speed_bits,
                                              double *tile_acc, const int32_t *status,
-                                             const int64_t *__restrict__ gbase,
                                              const int64_t *__restrict__ gplan) {
     // the status word is read now but tested only once this tile's staging
     // is in flight: testing it first put a dependent global load in front
@@ -550,10 +549,18 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     StepSmem<M> &s = *reinterpret_cast<StepSmem<M> *>(smem_raw);
     const int t = threadIdx.x;
     const int tile = blockIdx.x;
-    const int p = tiles[3 * tile];
-    const int tj0 = tiles[3 * tile + 1];
-    const int ti0 = tiles[3 * tile + 2];
-    const PatchView pv = patch_view(lv, p);
+    // one 32-byte descriptor (k_make_desc) instead of the chain tile list ->
+    // box/offset -> ghost base: one L2 round trip in front of the staging
+    const int4 dq0 = __ldg(reinterpret_cast<const int4 *>(desc + tile));
+    const int4 dq1 = __ldg(reinterpret_cast<const int4 *>(desc + tile) + 1);
+    const int p = dq0.x, tj0 = dq0.y, ti0 = dq0.z;
+    PatchView pv;
+    pv.nx = dq0.w & 0xffff;
+    pv.ny = dq0.w >> 16;
+    pv.NX = pv.nx + 2 * MLAMR_G;
+    pv.NY = pv.ny + 2 * MLAMR_G;
+    pv.off = (int64_t)(((unsigned long long)(unsigned)dq1.y << 32) | (unsigned)dq1.x);
+    const int64_t gb = (int64_t)(((unsigned long long)(unsigned)dq1.w << 32) | (unsigned)dq1.z);
     const int ty = min(TY, pv.ny - tj0);
     const int tx = min(TX, pv.nx - ti0);
     const int ny2 = ty + 2, nx2 = tx + 2;
@@ -599,7 +606,7 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
                     else
                         gi = 4 * pv.NX + (J - MLAMR_G) * 4 + (I < MLAMR_G ? I : I - pv.NX + 4);
                     fr[i] = true;
-                    gv[i] = gplan[gbase[p] + gi];
+                    gv[i] = gplan[gb + gi];
                 }
             }
         }
@@ -787,9 +794,9 @@ __global__ void __launch_bounds__(NTF) k_max_speed(mlamr_level lv, const double 
 
 template <int M>
 static int launch_step(const mlamr_level &lv, const double *src, double *dst,
-                       const int32_t *tiles, int n_tiles, double dt, int y_first,
+                       const TileDesc *desc, int n_tiles, double dt, int y_first,
                        const mlamr_params &prm, long long *speed_bits, double *tile_acc,
-                       const int32_t *status, const int64_t *gbase, const int64_t *gplan, cudaStream_t st) {
+                       const int32_t *status, const int64_t *gplan, cudaStream_t st) {
     const size_t smem = sizeof(StepSmem<M>);
     // the shared-memory opt-in is a per-device function attribute
     constexpr int kMaxDev = 64;
@@ -822,11 +829,11 @@ static int launch_step(const mlamr_level &lv, const double *src, double *dst,
             kc.rr[a][b] = (a < b && b < M) ? prm.densities[a] / prm.densities[b] : 0.0;
     kc.coef = (M > 1) ? prm.gravity * (1.0 - kc.rr[0][1]) : 0.0;
     if (y_first)
-        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status,
-                                                   gbase, gplan);
+        k_step<M, true><<<n_tiles, NT, smem, st>>>(lv, src, dst, desc, dt, prm, kc, speed_bits, tile_acc, status,
+                                                   gplan);
     else
-        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, tiles, dt, prm, kc, speed_bits, tile_acc, status,
-                                                    gbase, gplan);
+        k_step<M, false><<<n_tiles, NT, smem, st>>>(lv, src, dst, desc, dt, prm, kc, speed_bits, tile_acc, status,
+                                                    gplan);
     return (int)cudaGetLastError();
 }
 
