@@ -289,9 +289,13 @@ def b200_arm(args):
     sim.host_prof.clear()
     from paper_1803_01450_b200 import device as _D
     _D.POOL_PROF.clear()
+    # only the finest step launches carry events inside the timed region (16
+    # pairs per coarse step); the auxiliary kernels' per-launch events and
+    # byte accounting cost ~4 ms per C4 coarse step (tools/gap_ab.py) and run
+    # in a pass of their own after it
     sim.step_timer_level = L
     sim.step_events = []
-    sim.kernel_timer = {}
+    sim.kernel_timer = None
     launches0 = N.LAUNCHES[0]
     cells0 = sim.stats.total_cell_updates
     xbytes0 = getattr(sim, "bytes_exchanged", 0)
@@ -349,14 +353,27 @@ def b200_arm(args):
     achieved = (sum(byts) / sum(durs)) / 1e9 if durs else None
     step_share = sum(durs) / (ms * 1e-3) if durs else None
     sim.step_timer_level = None
-    kernels = kernel_rooflines(sim.kernel_timer, peak, ms * 1e-3)
-    sim.kernel_timer = None
     pool_bytes = sum(p.state.numel() * 8 * 2 + p.bathy.numel() * 8 for p in sim.levels.values())
     patches_per_level = ({str(k): int(len(v)) for k, v in sim.layout.items()}
                          if world > 1 else {str(k): v.P for k, v in sim.levels.items()})
     cells_per_level = {str(k): v.ncells for k, v in sim.levels.items()}
     host_ms = {k: round(1e3 * v / args.steps, 2) for k, v in sim.host_prof.items()}
     xbytes = int((getattr(sim, "bytes_exchanged", 0) - xbytes0) / args.steps)
+    # ---- auxiliary kernels: an instrumented pass outside the timed region ----
+    kernels = None
+    if not args.no_aux:
+        sim.kernel_timer = {}
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        n_aux = max(1, min(args.steps, 10))
+        for _ in range(n_aux):
+            coarse_step(sim)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        kernels = kernel_rooflines(sim.kernel_timer, peak, a0.elapsed_time(a1) * 1e-3)
+        sim.kernel_timer = None
 
     # ---- regrid stress (C5s), single GPU --------------------------------------
     stress = None
@@ -464,6 +481,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-stress", action="store_true", help="skip the C5s regrid-stress measurement")
+    ap.add_argument("--no-aux", action="store_true",
+                    help="skip the auxiliary kernels' instrumented pass (kernels_roofline)")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)
