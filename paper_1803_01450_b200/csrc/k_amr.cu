@@ -719,6 +719,41 @@ __global__ void __launch_bounds__(NTR, NTR == NTA ? MLAMR_RG_MINB : 1) k_regrid_
     constexpr int RG = 4;
     const int ncell = nv.nx * nv.ny;
     const int stride = gridDim.x * NTR;
+    // A new patch whose box is an old patch's box (most of a level away from
+    // the moving front) is that patch: its interior rows, side frame columns
+    // included, are one contiguous range per plane in both layouts, copied
+    // flat -- no owner lookups, no row split.  (The frame columns are
+    // refilled before anything reads them.)
+    {
+        const int o0 = owner_at(ol.own, ol.level_nx, ol.level_ny, nv.lo_i, nv.lo_j);
+        bool same = false;
+        if (o0 >= 0) {
+            const int32_t *b = ol.box + 4 * o0;
+            same = b[0] == nv.lo_i && b[1] == nv.lo_j && b[2] - b[0] + 1 == nv.nx && b[3] - b[1] + 1 == nv.ny;
+        }
+        if (same) {
+            const int64_t so = ol.offset[o0] + (int64_t)MLAMR_G * nv.NX, dof = nv.off + (int64_t)MLAMR_G * nv.NX;
+            const int n = nv.ny * nv.NX;
+            for (int base = blockIdx.x * NTR + threadIdx.x; base < n; base += RG * stride) {
+                double v[RG][3 * M];
+#pragma unroll
+                for (int u = 0; u < RG; ++u)
+                    if (base + u * stride < n)
+#pragma unroll
+                        for (int f = 0; f < 3 * M; ++f) v[u][f] = ol.state[f * OF + so + base + u * stride];
+#pragma unroll
+                for (int u = 0; u < RG; ++u)
+                    if (base + u * stride < n)
+#pragma unroll
+                        for (int f = 0; f < 3 * M; ++f) nl.state[f * NF + dof + base + u * stride] = v[u][f];
+            }
+            // nothing refined: the patch's refine delta is zero
+            if (threadIdx.x == 0)
+#pragma unroll
+                for (int m = 0; m < M; ++m) refine_delta[((int64_t)p * gridDim.x + blockIdx.x) * M + m] = 0.0;
+            return;
+        }
+    }
     for (int base = blockIdx.x * NTR + threadIdx.x; base < ncell; base += RG * stride) {
         int64_t ks[RG], kd[RG];
 #pragma unroll

@@ -143,17 +143,20 @@ static std::atomic<int> g_step_form{step_form_init()};
 static bool use_walker() { return g_step_form.load(std::memory_order_relaxed) == 1; }
 
 // Descriptor scratch, one per (device, stream), grown on demand: launches
-// on one stream are ordered, so reuse is safe.
+// on one stream are ordered, so reuse is safe -- provided a descriptor
+// build and the step launch that reads it enter the stream back to back.
+// The reference calls step_patch from a thread pool (driver.py:231-232), so
+// callers hold g_desc_mu from desc_scratch() until the step is launched.
+static std::mutex g_desc_mu;
 static TileDesc *desc_scratch(cudaStream_t st, int n_tiles) {
     struct Buf { TileDesc *p; int cap; };
-    static std::mutex mu;
     static std::map<std::pair<int, cudaStream_t>, Buf> pool;
     int dev = 0;
     cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(mu);
     Buf &b = pool[{dev, st}];
     if (b.cap < n_tiles) {
-        // the old buffer may still be read by a launch in flight on `st`
+        // the old buffer may still be read by a launch in flight on `st`:
+        // stream-ordered free
         if (b.p != nullptr) cudaFreeAsync(b.p, st);
         b.p = nullptr;
         b.cap = 0;
@@ -164,6 +167,7 @@ static TileDesc *desc_scratch(cudaStream_t st, int n_tiles) {
     return b.p;
 }
 
+// with g_desc_mu held
 static const TileDesc *make_desc(const mlamr_level &lv, const int32_t *tiles, int n_tiles, const int64_t *gbase,
                                  cudaStream_t st) {
     TileDesc *desc = desc_scratch(st, n_tiles);
@@ -291,6 +295,7 @@ static int launch_step_shape(int tile_tx, const mlamr_level &lv, const double *s
                              cudaStream_t st) {
     if (n_tiles <= 0) return 0;
     if (tile_tx == narrow::TX) {
+        std::lock_guard<std::mutex> lk(g_desc_mu);
         const TileDesc *desc = make_desc(lv, tiles, n_tiles, gbase, st);
         if (desc == nullptr) return -2;
         return narrow::launch_step<M>(lv, src, dst, desc, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,
@@ -302,6 +307,7 @@ static int launch_step_shape(int tile_tx, const mlamr_level &lv, const double *s
                                         status, gbase, gplan, st);
     }
     if (tile_tx == wide::TX) {
+        std::lock_guard<std::mutex> lk(g_desc_mu);
         const TileDesc *desc = make_desc(lv, tiles, n_tiles, gbase, st);
         if (desc == nullptr) return -2;
         return wide::launch_step<M>(lv, src, dst, desc, n_tiles, dt, y_first, prm, speed_bits, tile_acc, status,

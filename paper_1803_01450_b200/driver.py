@@ -140,11 +140,15 @@ class Simulation:
     (:mod:`paper_1803_01450_b200.problems`)."""
 
     def __init__(self, problem, device: str = "cuda", stream: torch.cuda.Stream | None = None,
-                 _restore: dict | None = None, reserve_factor: float = 1.0):
+                 _restore: dict | None = None, reserve_factor: float = 2.0):
         """``reserve_factor``: after the initial hierarchy is built, warm the
         device allocator with that multiple of its buffer bytes, so pools
         that grow at regrids do not pay cudaMalloc inside the time loop
-        (device.reserve)."""
+        (device.reserve).  A pool that outgrows its recycled buffers asks for
+        1.5x its size in one piece (~6.6 GB for C4's finest level); with a
+        factor of 1 that request found the warmed block already split in
+        some runs and cost an ~80 ms cudaMalloc inside the loop (4 ms per
+        coarse step of a 20-step bench), hence 2."""
         self._common_init(problem, device, stream)
         if _restore is not None:
             self._restore_from(_restore)

@@ -44,7 +44,7 @@ _EMPTY = np.zeros((0, 4), np.int64)
 
 class ShardedSimulation(Simulation):
     def __init__(self, problem, comm: Comm | None = None, device: str = "cuda", stream=None,
-                 reserve_factor: float = 1.0, _restore: dict | None = None):
+                 reserve_factor: float = 2.0, _restore: dict | None = None):
         self._init_sharding(comm)
         self._common_init(problem, device, stream)
         self._xstream = torch.cuda.Stream(device=self.dev)
