@@ -315,12 +315,15 @@ __device__ bool sweep_tile(StepSmem<M> &s, int ny2, int nx2, double dt, double d
                 const double FRh = hR * ur;
                 const double FLm = ((hL * ul) * ul) + (((0.5 * g) * hL) * hL);
                 const double FRm = ((hR * ur) * ur) + (((0.5 * g) * hR) * hR);
-                if (SL >= 0.0) {
-                    fh = FLh;
-                    fm = FLm;
-                } else if (SR <= 0.0) {
-                    fh = FRh;
-                    fm = FRm;
+                // the subsonic case first (nearly every interface): written as
+                // if / else-if / else, the compiler copied the left and the
+                // right state into the flux registers in front of each test
+                // (8 moves per layer on the common path).  NaN speeds fail
+                // both tests and take the HLL branch, as in the reference.
+                if (SL >= 0.0 || SR <= 0.0) {
+                    const bool left = SL >= 0.0;
+                    fh = left ? FLh : FRh;
+                    fm = left ? FLm : FRm;
                 } else {
                     const double den = SR - SL;
                     double djump;
