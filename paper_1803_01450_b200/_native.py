@@ -193,8 +193,10 @@ LAUNCHES = [0]
 
 
 def check(rc: int, what: str) -> None:
-    """Every C-ABI compute entry point launches exactly one kernel; count it."""
-    LAUNCHES[0] += 1
+    """Count the kernels a C-ABI compute entry point launches: one each,
+    except mlamr_step, which writes its tile descriptors first
+    (k_make_desc, csrc/k_step.cu)."""
+    LAUNCHES[0] += 2 if what in ("mlamr_step", "step") else 1
     if rc != 0:
         raise NativeLibraryError(f"{what} failed to launch (cuda error {rc})")
 

@@ -257,8 +257,9 @@ class Simulation:
         return self.specs[level - 1]
 
     def _call(self, fn, *args, what=""):
-        self.launches += 1
-        N.check(fn(*args), what or fn.__name__)
+        what = what or fn.__name__
+        self.launches += 2 if what == "mlamr_step" else 1   # + k_make_desc
+        N.check(fn(*args), what)
 
     # -- per-kernel timing for the bench (CUDA events on the driver stream) ------
     def _kt0(self):
