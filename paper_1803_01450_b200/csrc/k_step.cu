@@ -45,7 +45,7 @@ struct StepConst {
 // k_make_desc in front of each step launch (~2 us).
 struct __align__(16) TileDesc {
     int32_t p, tj0, ti0;  // patch, tile origin in the patch interior
-    int32_t nxy;          // patch interior nx | ny << 16
+    int32_t nxy;          // patch interior nx | ny << 16 (a patch side stays below 65,536 cells)
     int64_t off;          // patch offset in a field plane
     int64_t gb;           // ghost plan base of the patch (0 without a plan)
 };

@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(NT, MLAMR_STEP_MINB) k_step(mlamr_level lv, co
     const int p = dq0.x, tj0 = dq0.y, ti0 = dq0.z;
     PatchView pv;
     pv.nx = dq0.w & 0xffff;
-    pv.ny = dq0.w >> 16;
+    pv.ny = (int)((unsigned)dq0.w >> 16);
     pv.NX = pv.nx + 2 * MLAMR_G;
     pv.NY = pv.ny + 2 * MLAMR_G;
     pv.off = (int64_t)(((unsigned long long)(unsigned)dq1.y << 32) | (unsigned)dq1.x);
