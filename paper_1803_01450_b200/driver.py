@@ -153,7 +153,7 @@ class Simulation:
         if _restore is not None:
             self._restore_from(_restore)
         else:
-            base = self._new_pool(1, boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)]))
+            base = self._new_pool(1, self.level1_boxes())
             self._set_initial(base)
             self.levels[1] = base
             for lev in range(1, self.L):
@@ -164,6 +164,23 @@ class Simulation:
         if reserve_factor > 0:
             from .device import reserve
             reserve(int(reserve_factor * self.device_bytes()), self.dev, self.stream)
+
+    def level1_boxes(self, default_tile: int = 0) -> np.ndarray:
+        """Level 1's patches: the reference's single patch over the domain
+        (mesh.py:372-375), or -- ``MLAMR_L1_TILE=T`` -- aligned T x T tiles
+        of it.  Tiling is bit-exact (SURVEY.md App. C probe 4: a tile's halo
+        is its siblings' interior at the same time level, the domain edge's
+        ghost cells the same boundary conditions;
+        tests/test_gpu_driver.py::test_tiled_level1_is_bit_identical) and is
+        what lets a sharded run spread level 1 over the ranks instead of
+        giving it to rank 0."""
+        nx, ny = self.specs[0].nx, self.specs[0].ny
+        full = boxes_array([IndexBox(0, 0, nx - 1, ny - 1)])
+        T = int(os.environ.get("MLAMR_L1_TILE") or default_tile)
+        if T <= 0 or (T >= nx and T >= ny):
+            return full
+        from .regrid import chop_boxes
+        return np.asarray(chop_boxes(full, T, T, aligned=True), dtype=np.int64).reshape(-1, 4)
 
     def device_bytes(self) -> int:
         """Bytes of the level pools' state and bathymetry buffers."""

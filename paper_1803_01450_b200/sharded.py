@@ -53,11 +53,17 @@ class ShardedSimulation(Simulation):
         if _restore is not None:
             self._restore_from(_restore)
             return
-        b1 = boxes_array([IndexBox(0, 0, self.specs[0].nx - 1, self.specs[0].ny - 1)])
+        # level 1 as aligned tiles spread over the ranks like any other
+        # level (bit-identical to the reference's single level-1 patch:
+        # Simulation.level1_boxes); 128-cell tiles unless MLAMR_L1_TILE says
+        # otherwise (C4's 512^2 level 1: 16 tiles), one patch if the domain
+        # fits one tile or the job has one rank
+        b1 = self.level1_boxes(128 if self.world > 1 else 0)
+        layouts, owners = {1: b1}, {1: partition(b1, *self._scale(1), self.world)}
         self.layout[1] = b1
-        self.owner[1] = np.zeros(1, np.int32)
-        self.held[1] = {r: (np.arange(1) if r == 0 else np.zeros(0, np.int64)) for r in range(self.world)}
-        self.full[1] = {r: self.held[1][r].copy() for r in range(self.world)}
+        self.owner[1] = owners[1]
+        self.held[1] = self._held_all(1, layouts, owners)
+        self.full[1] = self._full_all(1, layouts, owners)
         base = self._make_pool(1, b1, self.owner[1], self.held[1][self.rank])
         self._set_initial(base)
         self.levels[1] = base
@@ -584,8 +590,16 @@ class ShardedSimulation(Simulation):
         if has_child:
             if ev is not None:
                 self.stream.wait_event(ev)
+            # (iii) in two halves around the t1 fill.  The fill copies
+            # sibling interiors into owned frames, and a boundary condition
+            # corner outside the domain is built from such a copied cell;
+            # the children's fills read that corner (through the ghost owner
+            # map) when their parent stencil leaves the domain next to a
+            # foreign sibling.  So the shadows' interiors must be at t1
+            # before the fill, and the parents' frames go out after it.
+            self._refresh(level)                                        # (iii-a)
             self.fill_level_ghosts(level, t1)
-            self._refresh(level)                                        # (iii)
+            self._refresh(level, full_only=True)                        # (iii-b)
             self._stash[level] = (t0, dt, pool.other)
             s = self.spec(level)
             dtf = dt / s.r_t

@@ -66,6 +66,12 @@ def main():
                     x, y = a[:, 2:-2, 2:-2], c[:, 2:-2, 2:-2]
                     if not np.array_equal(x, y):
                         bad += 1
+                        if os.environ.get("MLAMR_TEST_VERBOSE"):
+                            d = np.argwhere(x != y)
+                            print(f"rank {rank} {tag}: level {lev} patch {g} box {box} differs in {len(d)} cells, "
+                                  f"first {d[:4].tolist()}, max |diff| {np.nanmax(np.abs(x - y)):.3e}\n"
+                                  + "\n".join("".join(".X"[int(v)] for v in row) for row in (x != y).any(axis=0)),
+                                  flush=True)
         assert bad == 0, (tag, rank, bad)
 
     compare("init")

@@ -178,3 +178,44 @@ def test_walker_step_form_matches_oracle(oracle, name):
             assert compare_levels(gpu, cpu) == []
     finally:
         N.lib().mlamr_set_step_form(prev)
+
+
+def _level1_composite(sim):
+    """Level 1's interior cells on the full grid, whatever its patches."""
+    s = sim.spec(1)
+    out = None
+    for box, h, hu, hv, _ in sim.patch_fields(1):
+        if out is None:
+            out = np.full((3, h.shape[0], s.ny, s.nx), np.nan)
+        lo_i, lo_j, hi_i, hi_j = box
+        for q, a in enumerate((h, hu, hv)):
+            out[q, :, lo_j:hi_j + 1, lo_i:hi_i + 1] = a[:, 2:-2, 2:-2]
+    return out
+
+
+@pytest.mark.parametrize("name,tile", [("C2", 32), ("C3", 16), ("C4", 16), ("C5", 32)])
+def test_tiled_level1_is_bit_identical(monkeypatch, name, tile):
+    """Level 1 cut into aligned tiles (MLAMR_L1_TILE; what a sharded run
+    spreads over the ranks) steps bit for bit like the reference's single
+    level-1 patch (mesh.py:372-375; SURVEY.md App. C probe 4): same layouts
+    and fields on the finer levels, same level-1 cells, same dt."""
+    from paper_1803_01450_b200.driver import Simulation
+    pb, steps = _variant(name)
+    ref = Simulation(pb)
+    monkeypatch.setenv("MLAMR_L1_TILE", str(tile))
+    til = Simulation(pb)
+    monkeypatch.delenv("MLAMR_L1_TILE")
+    assert til.levels[1].P > 1 and ref.levels[1].P == 1
+    for _ in range(steps):
+        dt = ref.choose_dt()
+        assert til.choose_dt() == dt
+        for sim in (ref, til):
+            sim.apply_dynamic_rt(dt)
+            sim.advance_coarse_step(dt)
+        assert np.array_equal(_level1_composite(ref), _level1_composite(til))
+        for lev in range(2, ref.L + 1):
+            fa, fb = ref.patch_fields(lev), til.patch_fields(lev)
+            assert [x[0] for x in fa] == [x[0] for x in fb]
+            for x, y in zip(fa, fb):
+                for u, v in zip(x[1:4], y[1:4]):
+                    assert np.array_equal(u[:, 2:-2, 2:-2], v[:, 2:-2, 2:-2])

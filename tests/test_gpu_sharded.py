@@ -21,14 +21,20 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("name,overlap", [("C2", "0"), ("C2", "1"), ("C3", "0"), ("C4", "1"), ("C5", "0")])
-def test_sharded_two_ranks_match_single_gpu(name, overlap):
+@pytest.mark.parametrize("name,overlap,l1tile", [("C2", "0", "32"), ("C2", "1", "0"), ("C3", "0", "16"),
+                                                 ("C4", "1", "16"), ("C5", "0", "32")])
+def test_sharded_two_ranks_match_single_gpu(name, overlap, l1tile):
     """overlap = MLAMR_OVERLAP_REFRESH: the parents' refresh (ii) on its own
-    stream, overlapping the step."""
+    stream, overlapping the step.  l1tile = MLAMR_L1_TILE: level 1 cut into
+    tiles of that many cells a side and spread over the ranks ("0": the
+    single level-1 patch, owned by rank 0); the single-GPU run the worker
+    compares with uses the same level-1 layout, and
+    test_gpu_driver.py::test_tiled_level1_is_bit_identical ties that to the
+    untiled run."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(HERE, "dist_gpu_worker.py"), name]
-    env = dict(os.environ, MLAMR_OVERLAP_REFRESH=overlap)
+    env = dict(os.environ, MLAMR_OVERLAP_REFRESH=overlap, MLAMR_L1_TILE=l1tile)
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count("sharded == single-GPU") == 2, r.stdout[-2000:]
