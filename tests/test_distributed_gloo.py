@@ -185,3 +185,42 @@ def test_partition_balance_and_locality():
             b = B[own == r]
             area = (b[:, 2].max() - b[:, 0].min() + 1) * (b[:, 3].max() - b[:, 1].min() + 1)
             assert area <= 2.0 * 1024 * 1024 / world
+
+
+def test_tiled_level1_shadow_sets():
+    """Level 1 cut into tiles and spread over the ranks (sharded.py;
+    Simulation.level1_boxes): the tiles cover the domain exactly once, every
+    rank owns a share, and a rank holds -- besides its own tiles -- the
+    sibling tiles within its frames and every tile under the parent
+    stencils of its level-2 patches (so no rank needs all of level 1)."""
+    from paper_1803_01450_b200.distributed import G, coarsen_floor, grow, needed, partition
+    from paper_1803_01450_b200.regrid import chop_boxes
+    lay = _layouts()
+    full = lay[1]
+    tiles = np.asarray(chop_boxes(full.astype(np.int32), 16, 16, aligned=True), np.int64).reshape(-1, 4)
+    cover = np.zeros((64, 64), int)
+    for b in tiles:
+        assert b[0] % 16 == 0 and b[1] % 16 == 0
+        cover[b[1]:b[3] + 1, b[0]:b[2] + 1] += 1
+    assert len(tiles) == 16 and (cover == 1).all()
+    lay = dict(lay)
+    lay[1] = tiles
+    R = {1: (4, 4), 2: (4, 4)}
+    for world in (2, 4):
+        own = {lev: partition(b, 4 ** (3 - lev), 4 ** (3 - lev), world) for lev, b in lay.items()}
+        assert set(own[1]) == set(range(world))
+        fewer = False
+        for r in range(world):
+            held = needed(1, r, lay, own, R)
+            mine = np.flatnonzero(own[1] == r)
+            assert set(mine) <= set(held)
+            # every level-1 tile meeting the stencil of an owned level-2 patch
+            F = lay[2][own[2] == r]
+            st = grow(coarsen_floor(grow(F, G), 4, 4), 1)
+            for k, t in enumerate(tiles):
+                g = grow(t[None], G)[0]
+                hit = ((st[:, 0] <= g[2]) & (st[:, 2] >= g[0]) & (st[:, 1] <= g[3]) & (st[:, 3] >= g[1])).any()
+                if hit:
+                    assert k in held, (world, r, k)
+            fewer |= len(held) < len(tiles)
+        assert fewer or world == 2
