@@ -134,6 +134,11 @@ int mlamr_paint_owner(int32_t *map, int map_nx, int map_ny, const int32_t *box,
  * read from the sibling's interior directly, so the sibling copy of the
  * ghost fill need not run for this level (patches that need physical BCs
  * excepted: their BC corners read the copied frame).
+ * The call enqueues two kernels on `stream`: the work list expanded into
+ * 32-byte tile descriptors (library-owned scratch per device and stream,
+ * grown with the stream-ordered allocator), then the step.  Safe to call
+ * from several host threads, also on one stream (the reference steps its
+ * patches from a thread pool, driver.py:231-232).
  * Does nothing when *status != 0. */
 int mlamr_step(mlamr_level lv, const double *src_state, double *dst_state,
                const int32_t *tiles, int n_tiles, int tile_tx, double dt, int y_first,
